@@ -1,0 +1,249 @@
+/*
+ * vpb200.h -- C ABI of the B200-native ParaMaP mapping-and-planning hot path.
+ *
+ * Every entry point takes plain pointers and sizes (no torch types).  Pointers
+ * marked (dev) are CUDA device pointers owned by the caller; (host) pointers
+ * are read during the call only.  `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  Nothing here allocates device memory: scratch is passed in
+ * as a caller-owned workspace whose size the matching *_workspace_bytes()
+ * function reports.  Every function returns VPB_OK (0) or an error code;
+ * vpb_last_error() describes the most recent failure on the calling thread.
+ *
+ * The reference (/root/reference/pkg/src/voxplan, "vp/") has no formal plugin
+ * registry: its boundary is a set of module-level numba kernels looked up at
+ * call time.  Each entry below names the reference
+ * function it replaces; INTEGRATION.md shows the ctypes shim that binds it in
+ * place of the numba seam.
+ */
+#ifndef VPB200_H
+#define VPB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VPB_OK 0
+#define VPB_ERR_ARG 1  /* invalid argument (shape, limit, null pointer) */
+#define VPB_ERR_CUDA 2 /* CUDA launch / runtime error */
+
+#define VPB_MAX_JOINTS 16
+#define VPB_MAX_SPHERES 64
+#define VPB_MAX_PAIRS 256
+#define VPB_MAX_MASK_SPHERES 64
+
+int vpb_version(void);
+const char *vpb_last_error(void);
+/* Number of kernels this library has launched since load (diagnostics). */
+uint64_t vpb_launch_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* Mapping                                                                   */
+/* ------------------------------------------------------------------------ */
+
+/* Pinhole depth camera (vp/mapping.py:143-166, CameraModel). */
+typedef struct {
+  double fx, fy, cx, cy, d_min, d_max;
+  int64_t width, height;
+  double pose_r[9], pose_t[3]; /* camera -> world (cam.pose) */
+  double w2c_r[9], w2c_t[3];   /* world -> camera (cam.world_to_camera()) */
+} vpb_camera;
+
+/* Log-odds constants (vp/mapping.py:41-50, MapParams) and tau. */
+typedef struct {
+  double l_hit, l_miss, l_min, l_max, l_occ_threshold, tau;
+} vpb_map_params;
+
+/* Dense grid state: log_odds f64 and observed u8 over (gx, gy, gz), C order
+ * x*gy*gz + y*gz + z (vp/mapping.py:3-4).  occ_bits (optional) is the packed
+ * occupancy mask maintained next to the log-odds: bit (z & 31) of word
+ * (x*gy + y)*ceil(gz/32) + (z >> 5) is set iff log_odds >= l_occ_threshold. */
+typedef struct {
+  double *log_odds;   /* (dev) */
+  uint8_t *observed;  /* (dev) */
+  uint32_t *occ_bits; /* (dev) or NULL */
+  int64_t dims[3];
+  double origin[3];
+  double voxel;
+} vpb_grid;
+
+/* Number of uint32 words of the packed occupancy mask of a grid. */
+int64_t vpb_occ_words(const int64_t dims[3]);
+
+/* Rebuild occ_bits from log_odds over the whole grid (used after direct
+ * writes to log_odds).  Replaces the `grid.occupied_mask()` threshold of
+ * vp/mapping.py:113-114 / :601. */
+int vpb_occ_bits_from_log_odds(const vpb_grid *grid, double l_occ_threshold,
+                               void *stream);
+
+/* Pixels whose back-projection lies inside an inflated mask sphere.
+ * Replaces vp/mapping.py:357-380 (_masked_pixels).
+ * depth (dev) H x W f64; centers (host) n x 3; radii (host) n; out (dev) u8. */
+int vpb_masked_pixels(const double *depth, const vpb_camera *cam,
+                      const double *centers, const double *radii,
+                      int64_t n_mask, double pad, uint8_t *out, void *stream);
+
+/* Robot-masked voxel-projection fusion over box [lo, lo+n).
+ * Replaces vp/mapping.py:266-354 (_fuse_voxels, 29 args) -- bitwise equal
+ * log_odds / observed (fp64, reference operation order, no FMA).  When
+ * grid->occ_bits is non-NULL it is kept consistent with the new log-odds.
+ * depth (dev) H x W f64; pixel_masked (dev) H x W u8; centers/radii (host). */
+int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3],
+                    const int64_t n[3], const vpb_camera *cam,
+                    const double *depth, const uint8_t *pixel_masked,
+                    const double *centers, const double *radii,
+                    int64_t n_mask, const vpb_map_params *params, void *stream);
+
+/* Masked pixels + fusion in one call: vp/mapping.py:386-455
+ * (update_occupancy).  pixel_scratch (dev) holds H*W bytes. */
+int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3],
+                         const int64_t n[3], const vpb_camera *cam,
+                         const double *depth, const double *centers,
+                         const double *radii, int64_t n_mask, double mask_pad,
+                         const vpb_map_params *params, uint8_t *pixel_scratch,
+                         void *stream);
+
+/* Exact squared EDT of the occupied voxels of box [lo, lo+n).
+ * Replaces the body of vp/mapping.py:586-613 (edt_3d: threshold, the three
+ * _edt_pass_* FH passes of :458-550, and the inf mapping).  Output out_sq
+ * (dev) is f32 (n0, n1, n2) C order: exact integer squared voxel distances
+ * (exact in f32 up to 2^24), +inf everywhere iff the box holds no source.
+ * Source: grid->occ_bits when use_bits != 0 (must be current), else the
+ * log-odds threshold.  workspace (dev) >= vpb_edt3d_workspace_bytes(n). */
+size_t vpb_edt3d_workspace_bytes(const int64_t n[3]);
+int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3],
+              double l_occ_threshold, int use_bits, float *out_sq,
+              void *workspace, size_t workspace_bytes, void *stream);
+
+/* Distance field view (vp/mapping.py:556-583, DistanceField) consumed by the
+ * query and by the rollout kernel. */
+typedef struct {
+  const float *sq; /* (dev) (n0, n1, n2), NULL = no field (snap=None) */
+  int64_t n[3];
+  int64_t lo[3];
+  double origin[3];
+  double voxel;
+  double outside_default;
+} vpb_field;
+
+/* Batched distance query: replaces vp/mapping.py:616-710 (_query_metric /
+ * query_distance), evaluated in fp64 exactly as the reference.
+ * points (dev) count x 3 f64; out (dev) count f64. */
+int vpb_query_distance(const vpb_field *field, const double *points,
+                       int64_t count, double *out, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Planner                                                                   */
+/* ------------------------------------------------------------------------ */
+
+/* Packed robot + objective (vp/planner.py:461-499 Planner.__init__ packing,
+ * vp/planner.py:38-102 PlannerParams) plus the per-call state and goal.
+ * Spheres must be sorted by link (the Python host sorts and keeps sph_orig
+ * so outputs come back in the caller's sphere order). */
+typedef struct {
+  int32_t n_joints, n_spheres, n_pairs, horizon;
+  double dt;
+  double base_r[9], base_t[3];
+  double off_r[VPB_MAX_JOINTS * 9], off_t[VPB_MAX_JOINTS * 3];
+  double axes[VPB_MAX_JOINTS * 3];
+  int32_t sph_link[VPB_MAX_SPHERES];
+  int32_t sph_orig[VPB_MAX_SPHERES];
+  double sph_loc[VPB_MAX_SPHERES * 3], sph_r[VPB_MAX_SPHERES];
+  int32_t pairs[VPB_MAX_PAIRS * 2];
+  double goal_r[9], goal_t[3];
+  double pose_weight[36], terminal_weight[36];
+  double pos_lo[VPB_MAX_JOINTS], pos_hi[VPB_MAX_JOINTS];
+  double vel_lo[VPB_MAX_JOINTS], vel_hi[VPB_MAX_JOINTS];
+  double acc_lo[VPB_MAX_JOINTS], acc_hi[VPB_MAX_JOINTS];
+  double acc_limit[VPB_MAX_JOINTS]; /* |command| clip (vp/planner.py:618) */
+  double q_ref[VPB_MAX_JOINTS];
+  double q0[VPB_MAX_JOINTS], qd0[VPB_MAX_JOINTS];
+  double w_env, w_self, w_q, w_qd, w_qdd, w_s, w_ns, d_act;
+  double lam; /* softmin temperature (vp/planner.py:373-384) */
+} vpb_problem;
+
+#define VPB_PREC_F32 0 /* production: fp32 arithmetic, fp64 cost sums */
+#define VPB_PREC_F64 1 /* parity mode: fp64 end to end */
+
+#define VPB_DTYPE_F32 0
+#define VPB_DTYPE_F64 1
+
+/* Rollout + cost evaluation of M control sequences.
+ * Replaces vp/batch.py:161-336 (evaluate_batch, 49 args).
+ * controls (dev) M x H x n of `dtype`; `nominal` (dev, H x n, same dtype) is
+ * added to every sample when non-NULL (controls then hold perturbations).
+ * costs (dev) M f64, terms (dev) M x 6 f64, flags (dev) M u8 (1 = log-map
+ * singularity, cost = inf); traj_q/traj_qd (dev, M x (H+1) x n f64) and
+ * sphere_pos (dev, M x H x S x 3 f64) are optional (NULL = not stored). */
+int vpb_evaluate_batch(const vpb_problem *prob, const vpb_field *field,
+                       const void *controls, const void *nominal, int dtype,
+                       int64_t M, int precision, double *costs, double *terms,
+                       uint8_t *flags, double *traj_q, double *traj_qd,
+                       double *sphere_pos, void *stream);
+
+/* Softmin weights (vp/planner.py:373-384): w = exp(-(S - min S)/lam) / sum.
+ * costs (dev) M f64 -> weights (dev) M f64; stats (dev, 3 f64) receives
+ * [min, Z, nonfinite_count].  Fixed-order reduction (deterministic). */
+size_t vpb_soft_weights_workspace_bytes(int64_t M);
+int vpb_soft_weights(const double *costs, int64_t M, double lam,
+                     double *weights, double *stats, void *workspace,
+                     size_t workspace_bytes, void *stream);
+
+/* Weighted mean update (vp/planner.py:387-400): out = nominal + sum_m w_m eps_m.
+ * nominal (dev, H*n f64), eps (dev, M x H*n of dtype), weights (dev, M f64). */
+size_t vpb_update_controls_workspace_bytes(int64_t M, int64_t hn);
+int vpb_update_controls(const double *nominal, const void *eps, int dtype,
+                        const double *weights, int64_t M, int64_t hn,
+                        double *out, void *workspace, size_t workspace_bytes,
+                        void *stream);
+
+/* One fused SMPC iteration on this device's shard of samples
+ * (vp/planner.py:594-630 smpc_step minus sampling):
+ *   rollout of nominal + eps (M local samples) -> costs; per-CTA softmin
+ *   partials (local min m_c, Z_c = sum exp(-(S-m_c)/lam), N_c = sum w eps)
+ *   merged in fixed order into this shard's partial
+ *   part_out (dev) = [m_r, Z_r, N_r[H*n], count_nonfinite, best_index].
+ * The shard partial is what ranks exchange; a single
+ * device calls vpb_smpc_finish directly on its own partial. */
+size_t vpb_smpc_workspace_bytes(int64_t M, int64_t H, int64_t n);
+int64_t vpb_smpc_partial_len(int64_t H, int64_t n);
+int vpb_smpc_partial(const vpb_problem *prob, const vpb_field *field,
+                     const void *eps, int dtype, const double *nominal,
+                     int64_t M, int precision, double *costs, uint8_t *flags,
+                     double *part_out, void *workspace, size_t workspace_bytes,
+                     void *stream);
+
+/* Merge R shard partials (R x partial_len, dev, fixed rank order) and finish
+ * the step: U* = nominal + N/Z, then re-evaluate U* (M = 1) for the
+ * diagnostics, clip the command and shift the warm start
+ * (vp/planner.py:614-629).  out (dev) layout:
+ *   [U* (H*n), command (n), next_nominal (H*n), weighted_cost, terms[6],
+ *    best_cost, Z, nonfinite_count, best_index]
+ * (weighted_cost = +inf when the re-evaluation hits the log singularity). */
+int64_t vpb_smpc_out_len(int64_t H, int64_t n);
+size_t vpb_smpc_finish_workspace_bytes(int64_t n_parts, int64_t H, int64_t n);
+int vpb_smpc_finish(const vpb_problem *prob, const vpb_field *field,
+                    const double *partials, int64_t n_parts,
+                    const double *nominal, int precision, double *out,
+                    void *workspace, size_t workspace_bytes, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* Perturbation sampler (vp/planner.py:182-219)     */
+/* ------------------------------------------------------------------------ */
+/* Counter-based Philox4x32-10 stream keyed by (seed, sample index), standard
+ * normals, moving-average smoothing over `window` (rows scaled 1/sqrt(count)),
+ * times sigma[j]; sample 0 is the zero perturbation.  Statistically (not
+ * bitwise) equivalent to numpy's Philox stream.  m_offset = global index of
+ * local sample 0 (for sharded sampling).  out (dev) M x H x n of dtype. */
+int vpb_sample_perturbations(uint64_t seed, int64_t m_offset, int64_t M,
+                             int64_t H, int64_t n, int64_t window,
+                             const double *sigma, int dtype, void *out,
+                             void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VPB200_H */

@@ -246,3 +246,54 @@ def update_controls(nominal, eps, w):
 
 def cpu_count() -> int:
     return int(lib().vpo_max_threads()) if _lib is not None or _LIB_PATH.exists() else (os.cpu_count() or 1)
+
+
+# ---------------------------------------------------------------------------
+# sampler + full step (vp/planner.py:182-219, :594-630) -- numpy restatement
+# ---------------------------------------------------------------------------
+def smoothing_matrix(horizon: int, window: int) -> np.ndarray:
+    """vp/planner.py:182-196."""
+    if window <= 1:
+        return np.eye(horizon)
+    back, fwd = (window - 1) // 2, window // 2
+    a = np.zeros((horizon, horizon))
+    for k in range(horizon):
+        lo, hi = max(0, k - back), min(horizon, k + fwd + 1)
+        a[k, lo:hi] = 1.0
+        a[k] /= np.sqrt(hi - lo)
+    return a
+
+
+def sample_perturbations(samples: int, horizon: int, dof: int, sigma, window: int, rng_seed: int) -> np.ndarray:
+    """vp/planner.py:199-219: per-sample Philox stream keyed by (seed, m),
+    sample 0 = 0, moving-average smoothing, times sigma."""
+    eps = np.empty((samples, horizon, dof))
+    eps[0] = 0.0
+    seed = int(rng_seed) & 0xFFFFFFFFFFFFFFFF
+    for m in range(1, samples):
+        gen = np.random.Generator(np.random.Philox(key=np.array([seed, m], dtype=np.uint64)))
+        eps[m] = gen.standard_normal((horizon, dof))
+    if window > 1 and samples > 1:
+        eps = np.einsum("hk,mkn->mhn", smoothing_matrix(horizon, window), eps)
+    eps *= np.broadcast_to(np.asarray(sigma, dtype=float), (dof,))
+    return eps
+
+
+def smpc_step(args: dict, nominal, eps, lam: float, acc_limits):
+    """vp/planner.py:594-630 without the host FK diagnostics: evaluate ->
+    soft_weights -> update_controls -> re-evaluate U* -> clip/shift."""
+    nominal = _c(nominal)
+    controls = nominal[None] + eps
+    res = evaluate_batch(args, controls)
+    if res["flags"].any():
+        raise ValueError("degenerate rotation")
+    w = soft_weights(res["costs"], lam)
+    if abs(w.sum() - 1.0) > 1e-9:
+        raise ValueError("weights do not sum to one")
+    u = update_controls(nominal, eps, w)
+    weighted = evaluate_batch(args, u[None])
+    command = np.clip(u[0], -np.asarray(acc_limits), np.asarray(acc_limits))
+    next_nominal = np.vstack([u[1:], np.zeros((1, u.shape[1]))])
+    return {"u": u, "command": command, "next_nominal": next_nominal, "costs": res["costs"],
+            "weighted_cost": float(weighted["costs"][0]), "weighted_terms": weighted["terms"][0],
+            "best_cost": float(res["costs"].min())}

@@ -1,0 +1,41 @@
+// Library-wide state: error strings, launch counter, device properties.
+#include <cstdarg>
+
+#include "vpb_common.cuh"
+
+namespace vpb {
+
+static thread_local char g_err[512] = "";
+static std::atomic<uint64_t> g_launches{0};
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+int sm_count() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached = n > 0 ? n : 148;
+  }
+  return cached;
+}
+
+}  // namespace vpb
+
+extern "C" {
+
+int vpb_version(void) { return 1; }
+
+const char *vpb_last_error(void) { return vpb::g_err; }
+
+uint64_t vpb_launch_count(void) { return vpb::g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,302 @@
+// Robot-masked voxel-projection occupancy fusion (sm_100a).
+//
+// Replaces vp/mapping.py:266-354 (_fuse_voxels), vp/mapping.py:357-380
+// (_masked_pixels) and the occupancy threshold of vp/mapping.py:113-114.
+//
+// Parity: log_odds / observed are bitwise equal to the reference.  Every
+// floating-point operation is an explicit round-to-nearest intrinsic
+// (__dmul_rn / __dadd_rn / __ddiv_rn) in the reference's left-to-right order,
+// so no FMA can be contracted regardless of compiler flags.
+//
+// Layout: one thread per voxel, a warp covers 32 consecutive z of one (x, y)
+// line aligned to a 32-voxel word of the packed occupancy mask, so log_odds /
+// observed accesses are coalesced and the occupancy word is rebuilt with one
+// ballot.  Voxels outside the robot's bounding box skip the sphere test;
+// voxels whose projection misses the image touch no memory at all.
+#include "vpb_common.cuh"
+
+namespace vpb {
+
+struct FusionArgs {
+  double *log_odds;
+  uint8_t *observed;
+  uint32_t *occ_bits;  // may be null
+  int64_t gy, gz, words_z;
+  int64_t lo0, lo1, lo2, n0, n1, n2;
+  int64_t wz_begin, wz_count;  // z-words covering the box
+  double origin0, origin1, origin2, voxel;
+  double r[9], t[3];
+  double fx, fy, cx, cy, d_min, d_max;
+  int64_t width, height;
+  const double *depth;
+  const uint8_t *pixel_masked;
+  double tau, l_hit, l_miss, l_min, l_max, l_thr;
+  int n_mask;
+  double aabb_lo[3], aabb_hi[3];
+  double mc[VPB_MAX_MASK_SPHERES * 3];
+  double mr2[VPB_MAX_MASK_SPHERES];
+};
+
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+
+// grid: x = lo0 + blockIdx.y ... flattened: blockIdx.x over (i0, i1, zword)
+__global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ FusionArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t per_x = A.n1 * A.wz_count;
+  const int64_t total = A.n0 * per_x;
+  if (warp_global >= total) return;
+  const int64_t i0 = warp_global / per_x;
+  const int64_t rem = warp_global - i0 * per_x;
+  const int64_t i1 = rem / A.wz_count;
+  const int64_t wz = A.wz_begin + (rem - i1 * A.wz_count);
+  const int64_t x = A.lo0 + i0, y = A.lo1 + i1;
+  const int64_t z = wz * 32 + lane;
+  const bool in_box = (z >= A.lo2) && (z < A.lo2 + A.n2);
+  const int64_t g = (x * A.gy + y) * A.gz + z;
+
+  bool touched = false;  // this lane's log-odds changed / was written
+  double newval = 0.0;
+
+  if (in_box) {
+    // Voxel centre: origin + (i + 0.5) * voxel  (vp/mapping.py:306-308)
+    const double px = dadd(A.origin0, dmul(dadd((double)x, 0.5), A.voxel));
+    const double py = dadd(A.origin1, dmul(dadd((double)y, 0.5), A.voxel));
+    const double pz = dadd(A.origin2, dmul(dadd((double)z, 0.5), A.voxel));
+
+    // Robot mask (vp/mapping.py:310-325).  Conservative AABB pre-reject:
+    // the box is padded by 1e-9 m on the host so rounding in the bounds can
+    // never reject a voxel the exact strict-< test would accept.
+    bool masked = false;
+    if (A.n_mask > 0 && px >= A.aabb_lo[0] && px <= A.aabb_hi[0] && py >= A.aabb_lo[1] &&
+        py <= A.aabb_hi[1] && pz >= A.aabb_lo[2] && pz <= A.aabb_hi[2]) {
+      for (int s = 0; s < A.n_mask; ++s) {
+        const double dx = dsub(px, A.mc[3 * s + 0]);
+        const double dy = dsub(py, A.mc[3 * s + 1]);
+        const double dz = dsub(pz, A.mc[3 * s + 2]);
+        const double d2 = dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
+        if (d2 < A.mr2[s]) {
+          masked = true;
+          break;
+        }
+      }
+    }
+    if (masked) {
+      const double old = A.log_odds[g];
+      newval = old > 0.0 ? 0.0 : old;
+      if (old > 0.0) A.log_odds[g] = 0.0;
+      A.observed[g] = 1;
+      touched = true;
+    } else {
+      // Camera transform (vp/mapping.py:327-329): ((r0 px + r1 py) + r2 pz) + t
+      const double qx = dadd(dadd(dadd(dmul(A.r[0], px), dmul(A.r[1], py)), dmul(A.r[2], pz)), A.t[0]);
+      const double qy = dadd(dadd(dadd(dmul(A.r[3], px), dmul(A.r[4], py)), dmul(A.r[5], pz)), A.t[1]);
+      const double qz = dadd(dadd(dadd(dmul(A.r[6], px), dmul(A.r[7], py)), dmul(A.r[8], pz)), A.t[2]);
+      if (qz > 0.0) {
+        // u = fx * qx / qz + cx ; nearest pixel floor(u + 0.5) (:332-335)
+        const double u = dadd(__ddiv_rn(dmul(A.fx, qx), qz), A.cx);
+        const double v = dadd(__ddiv_rn(dmul(A.fy, qy), qz), A.cy);
+        const double uf = floor(dadd(u, 0.5));
+        const double vf = floor(dadd(v, 0.5));
+        if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
+          const int64_t pix = (int64_t)vf * A.width + (int64_t)uf;
+          const double measured = __ldg(A.depth + pix);
+          if (measured >= A.d_min && measured <= A.d_max && !__ldg(A.pixel_masked + pix)) {
+            const double diff = dsub(qz, measured);
+            int cls = 0;
+            if (fabs(diff) <= A.tau) cls = 1;                    // hit
+            else if (qz < dsub(measured, A.tau)) cls = 2;        // miss
+            if (cls) {
+              double value = dadd(A.log_odds[g], cls == 1 ? A.l_hit : A.l_miss);
+              if (value < A.l_min) value = A.l_min;
+              else if (value > A.l_max) value = A.l_max;
+              A.log_odds[g] = value;
+              A.observed[g] = 1;
+              newval = value;
+              touched = true;
+            }
+          }
+        }
+      }
+    }
+  }
+
+  if (A.occ_bits != nullptr) {
+    const unsigned touched_mask = __ballot_sync(kFull, touched);
+    if (touched_mask != 0u) {
+      const unsigned occ_mask = __ballot_sync(kFull, touched && newval >= A.l_thr);
+      if (lane == 0) {
+        uint32_t *w = A.occ_bits + (x * A.gy + y) * A.words_z + wz;
+        *w = (*w & ~touched_mask) | (occ_mask & touched_mask);
+      }
+    }
+  }
+}
+
+struct MaskPixArgs {
+  const double *depth;
+  uint8_t *out;
+  int64_t width, height;
+  double fx, fy, cx, cy, d_min, d_max;
+  double r[9], t[3];
+  int n_mask;
+  double pad;
+  double mc[VPB_MAX_MASK_SPHERES * 3];
+  double mr[VPB_MAX_MASK_SPHERES];
+};
+
+// vp/mapping.py:357-380, one thread per pixel.
+__global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constant__ MaskPixArgs A) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= A.width * A.height) return;
+  const int64_t vv = idx / A.width, uu = idx - vv * A.width;
+  const double d = A.depth[idx];
+  uint8_t inside = 0;
+  if (A.n_mask > 0 && d >= A.d_min && d <= A.d_max) {
+    const double z = d;
+    const double xx = dmul(__ddiv_rn(dsub((double)uu, A.cx), A.fx), z);
+    const double yy = dmul(__ddiv_rn(dsub((double)vv, A.cy), A.fy), z);
+    double p[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      p[j] = dadd(dadd(dadd(dmul(xx, A.r[3 * j + 0]), dmul(yy, A.r[3 * j + 1])), dmul(z, A.r[3 * j + 2])), A.t[j]);
+    for (int s = 0; s < A.n_mask; ++s) {
+      const double dx = dsub(p[0], A.mc[3 * s + 0]);
+      const double dy = dsub(p[1], A.mc[3 * s + 1]);
+      const double dz = dsub(p[2], A.mc[3 * s + 2]);
+      const double r = dadd(A.mr[s], A.pad);
+      if (dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)) < dmul(r, r)) inside = 1;
+    }
+  }
+  A.out[idx] = inside;
+}
+
+// occupancy bits from log_odds: one warp per 32-voxel word.
+__global__ void __launch_bounds__(256) occ_bits_kernel(const double *__restrict__ log_odds,
+                                                       uint32_t *__restrict__ bits, int64_t lines,
+                                                       int64_t gz, int64_t words_z, double thr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= lines * words_z) return;
+  const int64_t line = w / words_z, wz = w - line * words_z;
+  const int64_t z = wz * 32 + lane;
+  const bool occ = z < gz && log_odds[line * gz + z] >= thr;
+  const unsigned m = __ballot_sync(kFull, occ);
+  if (lane == 0) bits[w] = m;
+}
+
+}  // namespace vpb
+
+using namespace vpb;
+
+static int fill_mask(const double *centers, const double *radii, int64_t n_mask, double *mc,
+                     double *aabb_lo, double *aabb_hi) {
+  VPB_REQUIRE(n_mask >= 0 && n_mask <= VPB_MAX_MASK_SPHERES, "mask sphere count %lld outside [0, %d]",
+              (long long)n_mask, VPB_MAX_MASK_SPHERES);
+  VPB_REQUIRE(n_mask == 0 || (centers && radii), "mask centers/radii are null");
+  for (int k = 0; k < 3; ++k) {
+    aabb_lo[k] = 1e300;
+    aabb_hi[k] = -1e300;
+  }
+  for (int64_t s = 0; s < n_mask; ++s) {
+    for (int k = 0; k < 3; ++k) {
+      mc[3 * s + k] = centers[3 * s + k];
+      const double r = fabs(radii[s]);
+      aabb_lo[k] = fmin(aabb_lo[k], centers[3 * s + k] - r - 1e-9 - 1e-12 * fabs(centers[3 * s + k]));
+      aabb_hi[k] = fmax(aabb_hi[k], centers[3 * s + k] + r + 1e-9 + 1e-12 * fabs(centers[3 * s + k]));
+    }
+  }
+  return VPB_OK;
+}
+
+extern "C" {
+
+int64_t vpb_occ_words(const int64_t dims[3]) { return dims[0] * dims[1] * ceil_div(dims[2], 32); }
+
+int vpb_occ_bits_from_log_odds(const vpb_grid *grid, double thr, void *stream) {
+  VPB_REQUIRE(grid && grid->log_odds && grid->occ_bits, "grid/log_odds/occ_bits is null");
+  const int64_t lines = grid->dims[0] * grid->dims[1];
+  const int64_t wz = ceil_div(grid->dims[2], 32);
+  const int64_t warps = lines * wz;
+  if (warps == 0) return VPB_OK;
+  occ_bits_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, as_stream(stream)>>>(
+      grid->log_odds, grid->occ_bits, lines, grid->dims[2], wz, thr);
+  return check_launch("occ_bits_kernel");
+}
+
+int vpb_masked_pixels(const double *depth, const vpb_camera *cam, const double *centers,
+                      const double *radii, int64_t n_mask, double pad, uint8_t *out, void *stream) {
+  VPB_REQUIRE(depth && cam && out, "null argument to vpb_masked_pixels");
+  MaskPixArgs A;
+  memset(&A, 0, sizeof(A));
+  double lo[3], hi[3];
+  int rc = fill_mask(centers, radii, n_mask, A.mc, lo, hi);
+  if (rc) return rc;
+  for (int64_t s = 0; s < n_mask; ++s) A.mr[s] = radii[s];
+  A.depth = depth;
+  A.out = out;
+  A.width = cam->width;
+  A.height = cam->height;
+  A.fx = cam->fx; A.fy = cam->fy; A.cx = cam->cx; A.cy = cam->cy;
+  A.d_min = cam->d_min; A.d_max = cam->d_max;
+  memcpy(A.r, cam->pose_r, sizeof(A.r));
+  memcpy(A.t, cam->pose_t, sizeof(A.t));
+  A.n_mask = (int)n_mask;
+  A.pad = pad;
+  const int64_t npx = cam->width * cam->height;
+  if (npx == 0) return VPB_OK;
+  masked_pixels_kernel<<<(unsigned)ceil_div(npx, 256), 256, 0, as_stream(stream)>>>(A);
+  return check_launch("masked_pixels_kernel");
+}
+
+int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
+                    const double *depth, const uint8_t *pixel_masked, const double *centers,
+                    const double *radii, int64_t n_mask, const vpb_map_params *p, void *stream) {
+  VPB_REQUIRE(grid && grid->log_odds && grid->observed && cam && depth && pixel_masked && p,
+              "null argument to vpb_fuse_voxels");
+  for (int k = 0; k < 3; ++k)
+    VPB_REQUIRE(lo[k] >= 0 && n[k] >= 1 && lo[k] + n[k] <= grid->dims[k], "box outside grid on axis %d", k);
+  FusionArgs A;
+  memset(&A, 0, sizeof(A));
+  int rc = fill_mask(centers, radii, n_mask, A.mc, A.aabb_lo, A.aabb_hi);
+  if (rc) return rc;
+  for (int64_t s = 0; s < n_mask; ++s) A.mr2[s] = radii[s] * radii[s];
+  A.log_odds = grid->log_odds;
+  A.observed = grid->observed;
+  A.occ_bits = grid->occ_bits;
+  A.gy = grid->dims[1];
+  A.gz = grid->dims[2];
+  A.words_z = ceil_div(grid->dims[2], 32);
+  A.lo0 = lo[0]; A.lo1 = lo[1]; A.lo2 = lo[2];
+  A.n0 = n[0]; A.n1 = n[1]; A.n2 = n[2];
+  A.wz_begin = lo[2] / 32;
+  A.wz_count = (lo[2] + n[2] - 1) / 32 - A.wz_begin + 1;
+  A.origin0 = grid->origin[0]; A.origin1 = grid->origin[1]; A.origin2 = grid->origin[2];
+  A.voxel = grid->voxel;
+  memcpy(A.r, cam->w2c_r, sizeof(A.r));
+  memcpy(A.t, cam->w2c_t, sizeof(A.t));
+  A.fx = cam->fx; A.fy = cam->fy; A.cx = cam->cx; A.cy = cam->cy;
+  A.d_min = cam->d_min; A.d_max = cam->d_max;
+  A.width = cam->width; A.height = cam->height;
+  A.depth = depth;
+  A.pixel_masked = pixel_masked;
+  A.tau = p->tau; A.l_hit = p->l_hit; A.l_miss = p->l_miss;
+  A.l_min = p->l_min; A.l_max = p->l_max; A.l_thr = p->l_occ_threshold;
+  A.n_mask = (int)n_mask;
+  const int64_t warps = A.n0 * A.n1 * A.wz_count;
+  fuse_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, as_stream(stream)>>>(A);
+  return check_launch("fuse_kernel");
+}
+
+int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
+                         const double *depth, const double *centers, const double *radii, int64_t n_mask,
+                         double mask_pad, const vpb_map_params *params, uint8_t *pixel_scratch, void *stream) {
+  VPB_REQUIRE(pixel_scratch, "pixel scratch is null");
+  int rc = vpb_masked_pixels(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, stream);
+  if (rc) return rc;
+  return vpb_fuse_voxels(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// Shared helpers for the sm_100a kernels behind include/vpb200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+
+#include "vpb200.h"
+
+namespace vpb {
+
+// Thread-local last-error message (vpb_last_error).
+void set_error(const char *fmt, ...);
+void note_launch(int n = 1);
+
+inline int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: %s", what, cudaGetErrorString(e));
+    return VPB_ERR_CUDA;
+  }
+  note_launch();
+  return VPB_OK;
+}
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+__host__ __device__ __forceinline__ int64_t vmin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t vmax64(int64_t a, int64_t b) { return a > b ? a : b; }
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+constexpr int kWarp = 32;
+constexpr unsigned kFull = 0xffffffffu;
+
+// Number of SMs of the current device (cached per process).
+int sm_count();
+
+}  // namespace vpb
+
+#define VPB_REQUIRE(cond, ...)      \
+  do {                              \
+    if (!(cond)) {                  \
+      ::vpb::set_error(__VA_ARGS__); \
+      return VPB_ERR_ARG;           \
+    }                               \
+  } while (0)
+
+#define VPB_CUDA(call)                                                       \
+  do {                                                                       \
+    cudaError_t _e = (call);                                                 \
+    if (_e != cudaSuccess) {                                                 \
+      ::vpb::set_error("%s failed: %s", #call, cudaGetErrorString(_e));      \
+      return VPB_ERR_CUDA;                                                   \
+    }                                                                        \
+  } while (0)

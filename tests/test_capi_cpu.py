@@ -1,0 +1,98 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads without a GPU
+and exports every entry point include/vpb200.h declares (no compute calls)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2512_22575_b200 import _lib, build
+
+    build.build()
+    return _lib.load()
+
+
+def header_functions():
+    text = (ROOT / "include" / "vpb200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*[a-z_0-9 ]+?\*?\s*\b(vpb_[a-z0-9_]+)\s*\(", text, flags=re.M)))
+
+
+def test_header_declares_the_boundary():
+    names = header_functions()
+    for want in ("vpb_fuse_voxels", "vpb_masked_pixels", "vpb_edt3d", "vpb_query_distance",
+                 "vpb_evaluate_batch", "vpb_soft_weights", "vpb_update_controls", "vpb_smpc_partial",
+                 "vpb_smpc_finish", "vpb_sample_perturbations"):
+        assert want in names
+
+
+def test_library_exports_every_header_symbol(lib):
+    from paper_2512_22575_b200 import _lib
+
+    for name in header_functions():
+        assert hasattr(lib, name), f"{name} declared in vpb200.h but not exported"
+        assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
+
+
+def test_library_is_sm100a(lib):
+    from paper_2512_22575_b200 import _lib
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_pure_host_entry_points(lib):
+    """Size queries are host-only and callable without a device."""
+    from paper_2512_22575_b200._lib import i64x3
+
+    assert lib.vpb_version() == 1
+    assert lib.vpb_occ_words(i64x3((4, 5, 33))) == 4 * 5 * 2
+    assert lib.vpb_edt3d_workspace_bytes(i64x3((8, 8, 8))) >= 8 * 8 * 8 * 6
+    assert lib.vpb_smpc_partial_len(32, 7) == 4 + 224
+    assert lib.vpb_smpc_out_len(32, 7) == 2 * 224 + 7 + 11
+
+
+def test_struct_layout_matches_header(lib):
+    """ctypes mirrors of the C structs have the C sizes (compiled probe)."""
+    import subprocess, tempfile
+    from paper_2512_22575_b200 import _lib
+
+    src = '#include <stdio.h>\n#include "vpb200.h"\nint main(){printf("%zu %zu %zu %zu %zu\\n", sizeof(vpb_camera), sizeof(vpb_map_params), sizeof(vpb_grid), sizeof(vpb_field), sizeof(vpb_problem));}'
+    with tempfile.TemporaryDirectory() as d:
+        c = Path(d) / "probe.c"
+        c.write_text(src)
+        exe = Path(d) / "probe"
+        r = subprocess.run(["gcc", "-I", str(ROOT / "include"), str(c), "-o", str(exe)], capture_output=True, text=True)
+        if r.returncode != 0:
+            pytest.skip("no C compiler")
+        sizes = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    want = [ctypes.sizeof(t) for t in (_lib.VpbCamera, _lib.VpbMapParams, _lib.VpbGrid, _lib.VpbField, _lib.VpbProblem)]
+    assert sizes == want
+
+
+def test_product_has_no_cpu_fallback():
+    """Without CUDA the product path raises instead of computing on the CPU."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("CUDA present")
+    from paper_2512_22575_b200 import mapping
+    from paper_2512_22575_b200._lib import NativeError
+
+    with pytest.raises(NativeError):
+        mapping.VoxelGrid((0, 0, 0), 0.1, (4, 4, 4))
+
+
+def test_product_never_imports_oracle():
+    for path in (ROOT / "paper_2512_22575_b200").rglob("*.py"):
+        text = path.read_text()
+        assert "import oracle" not in text and "from oracle" not in text, path

@@ -1,0 +1,317 @@
+"""GPU parity of the SMPC kernels (rollout/cost, softmin, update, smpc_step).
+
+Bars (BASELINE.json north_star):
+  * fp64 parity mode vs the reference golden vectors: rtol 1e-9 (the
+    reference's own batch-vs-scalar bar, t/test_planner.py:304-335);
+  * fp32 production mode: costs and the six terms within 1e-4 relative
+    (absolute floor 1e-4 * (1 + total cost) per sample for terms that are
+    tiny next to the total); weights |dw| <= 1e-4 * max w; U* within 1e-4
+    relative (floor 1e-6).
+The reference's own seeded noise (stored in the golden files) is fed to both
+sides.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import i32_to_sq, load_golden
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+KEYS = (
+    "q0 qd0 dt base_r base_t off_r off_t axes sph_link sph_loc sph_r pairs goal_r goal_t "
+    "pose_weight terminal_weight pos_lo pos_hi vel_lo vel_hi acc_lo acc_hi w_env w_self w_q "
+    "w_qd w_qdd w_s w_ns d_act q_ref field_sq field_lo0 field_lo1 field_lo2 field_origin0 "
+    "field_origin1 field_origin2 field_voxel field_outside"
+).split()
+
+
+@pytest.fixture(scope="module")
+def pk():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_22575_b200 as pkg
+    from paper_2512_22575_b200 import config, mapping, planner, robot
+
+    return pkg, config, mapping, planner, robot
+
+
+def _setup(pk, g, i, precision):
+    """Build Planner/state/goal/field for golden rollout case i from the
+    stored packed arguments (same robot, same objective)."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.geometry import RigidTransform, Rotation3
+
+    chain, model = config.robot_7dof()
+    prm = g[f"r_params_{i}"]
+    h, m, dt, lam, win, margin = prm
+    overrides = {"horizon": int(h), "samples": int(m), "dt": float(dt), "lam": float(lam),
+                 "noise_window": int(win), "margin_frac": float(margin), "q_ref": g[f"r_q_ref_{i}"],
+                 "pose_weight": g[f"r_pose_weight_{i}"], "terminal_weight": g[f"r_terminal_weight_{i}"]}
+    params = config.planner_params(7, overrides)
+    pl = planner.Planner(chain, model, params, precision=precision)
+    P = planner.pack_problem(chain, model, params)
+    for k in ("pos_lo", "pos_hi", "vel_lo", "vel_hi", "acc_lo", "acc_hi"):
+        np.testing.assert_array_equal(np.array(getattr(P, k)[:7]), g[f"r_{k}_{i}"])
+    state = robot.JointState(g[f"r_q0_{i}"], g[f"r_qd0_{i}"], np.zeros(7))
+    goal = RigidTransform(Rotation3(g[f"r_goal_r_{i}"]), g[f"r_goal_t_{i}"])
+    field = None
+    if f"r_grid_occ_{i}" in g:
+        sq = i32_to_sq(g[f"r_field_sq_{i}"])
+        shape = tuple(int(v) for v in g[f"r_field_shape_{i}"])
+        box = mapping.VoxelBox((0, 0, 0), shape)
+        field = mapping.DistanceField(g[f"r_grid_origin_{i}"], float(g[f"r_grid_voxel_{i}"]), shape, box,
+                                      torch.from_numpy(sq.astype(np.float32)).cuda(), float(g[f"r_field_outside_{i}"]))
+    return pl, state, goal, field
+
+
+def test_rollout_fp64_vs_golden(pk):
+    g = load_golden("rollout")
+    from paper_2512_22575_b200.errors import DegenerateRotation
+
+    for i in range(int(g["r_count"])):
+        name = str(g[f"r_name_{i}"])
+        pl, state, goal, field = _setup(pk, g, i, "fp64")
+        store = bool(g[f"r_store_{i}"])
+        ctrl = g[f"r_controls_{i}"]
+        flags = g[f"r_flags_{i}"]
+        if flags.any():
+            with pytest.raises(DegenerateRotation):
+                pl.evaluate(state, goal, field, ctrl)
+            costs, terms, fl, *_ = pl.evaluate_device(state, goal, field, torch.from_numpy(ctrl).cuda())
+            np.testing.assert_array_equal(fl.cpu().numpy(), flags, err_msg=name)
+            continue
+        res = pl.evaluate(state, goal, field, ctrl, keep_trajectories=store, keep_spheres=store)
+        np.testing.assert_allclose(res.costs, g[f"r_costs_{i}"], rtol=1e-9, err_msg=name)
+        np.testing.assert_allclose(res.terms, g[f"r_terms_{i}"], rtol=1e-9, atol=1e-9, err_msg=name)
+        if store:
+            np.testing.assert_allclose(res.traj_q, g[f"r_trajq_{i}"], rtol=1e-12, atol=1e-12, err_msg=name)
+            np.testing.assert_allclose(res.traj_qd, g[f"r_trajqd_{i}"], rtol=1e-12, atol=1e-12, err_msg=name)
+            np.testing.assert_allclose(res.sphere_positions, g[f"r_sphpos_{i}"], rtol=1e-11, atol=1e-12)
+
+
+def _fp32_close(got_costs, got_terms, want_costs, want_terms, name):
+    """costs: rtol 1e-4; each term: 1e-4 relative or 1e-6 of (1 + the
+    sample's total cost) absolute (terms that vanish next to the total)."""
+    np.testing.assert_allclose(got_costs, want_costs, rtol=1e-4, err_msg=name)
+    err = np.abs(got_terms - want_terms)
+    bound = 1e-4 * np.abs(want_terms) + 1e-6 * (1.0 + np.abs(want_costs))[:, None]
+    bad = err > bound
+    assert not bad.any(), f"{name}: fp32 terms off at {np.argwhere(bad)[:5]}: {got_terms[bad][:5]} vs {want_terms[bad][:5]}"
+
+
+def test_rollout_fp32_vs_golden(pk):
+    g = load_golden("rollout")
+    for i in range(int(g["r_count"])):
+        name = str(g[f"r_name_{i}"])
+        if g[f"r_flags_{i}"].any():
+            continue
+        pl, state, goal, field = _setup(pk, g, i, "fp32")
+        res = pl.evaluate(state, goal, field, g[f"r_controls_{i}"])
+        _fp32_close(res.costs, res.terms, g[f"r_costs_{i}"], g[f"r_terms_{i}"], name)
+
+
+def test_rollout_fp32_large_batch_vs_oracle(pk):
+    """C3 shape (M=4096, H=32) on the collision-free board scene against the
+    oracle (fp64 C restatement) on the same inputs."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200 import scene
+    from paper_2512_22575_b200.geometry import RigidTransform
+
+    chain, model = config.robot_7dof()
+    origin, voxel, occ = scene.reach_static_occupancy()
+    grid = mapping.VoxelGrid(origin, voxel, occ.shape)
+    grid.set_log_odds(np.where(occ, 3.5, 0.0))
+    field = mapping.edt_3d(grid, outside_default=0.8)
+    params = config.planner_params(7, {"samples": 4096, "horizon": 32, "q_ref": scene.REACH_STATIC_QREF})
+    state = robot.JointState.resting(scene.REACH_STATIC_START)
+    goal = RigidTransform.from_vec7(scene.REACH_STATIC_GOAL)
+    rng = np.random.default_rng(77)
+    ctrl = rng.normal(scale=1.5, size=(4096, 32, 7))
+    res = planner.Planner(chain, model, params, "fp32").evaluate(state, goal, field, ctrl)
+    args = _oracle_args(planner, chain, model, params, state, goal, field)
+    want = oracle.evaluate_batch(args, ctrl)
+    _fp32_close(res.costs, res.terms, want["costs"], want["terms"], "reach_static M=4096")
+    res64 = planner.Planner(chain, model, params, "fp64").evaluate(state, goal, field, ctrl)
+    np.testing.assert_allclose(res64.costs, want["costs"], rtol=1e-9)
+
+
+def _oracle_args(planner, chain, model, params, state, goal, field):
+    P = planner.pack_problem(chain, model, params)
+    lims = planner.tightened_limits(chain, params.margin_frac)
+    args = {
+        "q0": state.q, "qd0": state.qd, "dt": params.dt, "base_r": chain.base_pose.rotation.matrix,
+        "base_t": chain.base_pose.translation,
+        "off_r": np.array([j.parent_offset.rotation.matrix for j in chain.joints]),
+        "off_t": np.array([j.parent_offset.translation for j in chain.joints]),
+        "axes": np.array([j.axis for j in chain.joints]),
+        "sph_link": np.array([s.link for s in model.spheres]), "sph_loc": np.array([s.center for s in model.spheres]),
+        "sph_r": model.radii(), "pairs": np.array(model.self_pairs), "goal_r": goal.rotation.matrix,
+        "goal_t": goal.translation, "pose_weight": params.pose_weight, "terminal_weight": params.terminal_weight,
+        "w_env": params.w_env, "w_self": params.w_self, "w_q": params.w_q, "w_qd": params.w_qd,
+        "w_qdd": params.w_qdd, "w_s": params.w_s, "w_ns": params.w_ns, "d_act": params.d_act, "q_ref": params.q_ref,
+    }
+    for k, v in zip(("pos_lo", "pos_hi", "vel_lo", "vel_hi", "acc_lo", "acc_hi"), lims):
+        args[k] = v
+    del P
+    if field is None:
+        args.update(field_sq=np.full((1, 1, 1), np.inf), field_lo0=2**40, field_lo1=2**40, field_lo2=2**40,
+                    field_origin0=0.0, field_origin1=0.0, field_origin2=0.0, field_voxel=1.0, field_outside=np.inf)
+    else:
+        args.update(field_sq=field.sq, field_lo0=field.volume.lo[0], field_lo1=field.volume.lo[1],
+                    field_lo2=field.volume.lo[2], field_origin0=field.origin[0], field_origin1=field.origin[1],
+                    field_origin2=field.origin[2], field_voxel=field.voxel_size, field_outside=field.outside_default)
+    return args
+
+
+def test_softmin_update_vs_golden(pk):
+    pkg, config, mapping, planner, robot = pk
+    g = load_golden("softmin")
+    for i in range(int(g["s_count"])):
+        w = planner.soft_weights(g[f"s_costs_{i}"], float(g[f"s_lam_{i}"]))
+        np.testing.assert_allclose(w, g[f"s_w_{i}"], rtol=1e-12, atol=1e-300)
+        u = planner.update_controls(g[f"s_nom_{i}"], g[f"s_eps_{i}"], g[f"s_w_{i}"])
+        np.testing.assert_allclose(u, g[f"s_u_{i}"], rtol=1e-12, atol=1e-13)
+
+
+def test_softmin_errors(pk):
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.errors import WeightMismatch
+
+    with pytest.raises(ValueError):
+        planner.soft_weights(np.array([]), 0.5)
+    with pytest.raises(ValueError):
+        planner.soft_weights(np.array([1.0, np.inf]), 0.5)
+    with pytest.raises(ValueError):
+        planner.soft_weights(np.array([1.0]), 0.0)
+    with pytest.raises(WeightMismatch):
+        planner.update_controls(np.zeros((1, 1)), np.zeros((2, 1, 1)), np.array([0.6, 0.6]))
+    # dyadic shift invariance holds bitwise (t/test_planner.py:369-377)
+    rng = np.random.default_rng(7)
+    costs = rng.integers(0, 2**16, size=32).astype(float) / 1024.0
+    a = planner.soft_weights(costs, 0.31)
+    for shift in (1.0, 64.0, -17.5):
+        np.testing.assert_array_equal(planner.soft_weights(costs + shift, 0.31), a)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_smpc_step_vs_golden(pk, precision):
+    """Full smpc_step with the reference's noise (golden st_*)."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.geometry import RigidTransform, Rotation3
+    from conftest import unpack_occ
+
+    g = load_golden("softmin")
+    chain, model = config.robot_7dof()
+    occ = unpack_occ(g["st_grid_occ"], (30, 30, 30))
+    grid = mapping.VoxelGrid((-1.0, -1.0, 0.0), 0.05, (30, 30, 30))
+    grid.set_log_odds(np.where(occ, 3.5, 0.0))
+    field = mapping.edt_3d(grid, outside_default=0.8)
+    for j in range(int(g["st_count"])):
+        m, h, seed = (int(v) for v in g[f"st_cfg_{j}"])
+        params = config.planner_params(7, {"samples": m, "horizon": h})
+        pl = planner.Planner(chain, model, params, precision=precision)
+        state = robot.JointState(g[f"st_q0_{j}"], g[f"st_qd0_{j}"], np.zeros(7))
+        goal = RigidTransform(Rotation3(g[f"st_goal_r_{j}"]), g[f"st_goal_t_{j}"])
+        res = pl.smpc_step(state, goal, field, g[f"st_nominal_{j}"], seed, perturbations=g[f"st_eps_{j}"])
+        diag = g[f"st_diag_{j}"]
+        tol = 1e-9 if precision == "fp64" else 1e-4
+        floor = 1e-12 if precision == "fp64" else 1e-6
+        np.testing.assert_allclose(res.command, g[f"st_command_{j}"], rtol=tol, atol=floor)
+        np.testing.assert_allclose(res.next_nominal, g[f"st_next_{j}"], rtol=tol, atol=floor)
+        np.testing.assert_allclose(res.diagnostics.best_cost, diag[0], rtol=tol)
+        np.testing.assert_allclose(res.diagnostics.weighted_cost, diag[1], rtol=tol)
+        np.testing.assert_allclose(res.diagnostics.e_pos, diag[2], rtol=1e-12)
+        np.testing.assert_allclose(res.diagnostics.e_ori, diag[3], rtol=1e-9, atol=1e-12)
+
+
+def test_smpc_shard_merge_equals_single(pk):
+    """Sharded partials (2 and 8 shards of one batch) merged in rank order
+    equal the single-device step."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.geometry import RigidTransform
+
+    chain, model = config.robot_7dof()
+    params = config.planner_params(7, {"samples": 1024, "horizon": 20})
+    pl = planner.Planner(chain, model, params, "fp32")
+    state = robot.JointState.resting(np.full(7, 0.1))
+    goal = RigidTransform.from_vec7([0.3, -0.2, 0.7, 0.9, 0.1, 0.3, -0.2])
+    nom = torch.zeros((20, 7), dtype=torch.float64, device="cuda")
+    eps = pl.sample_device(123)
+    part1, costs, _ = pl.smpc_partial_device(state, goal, None, nom, eps)
+    single = pl.smpc_finish_device(state, goal, None, nom, part1.reshape(1, -1)).cpu().numpy()
+    for shards in (2, 8):
+        parts = []
+        step = 1024 // shards
+        for r in range(shards):
+            p, c, _ = pl.smpc_partial_device(state, goal, None, nom, eps[r * step:(r + 1) * step].contiguous())
+            torch.testing.assert_close(c, costs[r * step:(r + 1) * step], rtol=0, atol=0)
+            parts.append(p)
+        merged = pl.smpc_finish_device(state, goal, None, nom, torch.stack(parts)).cpu().numpy()
+        np.testing.assert_allclose(merged, single, rtol=1e-12, atol=1e-14)
+    # and the merged U* equals the explicit softmin + weighted mean on the same costs
+    w = planner.soft_weights(costs, params.lam)
+    u = planner.update_controls(nom, eps.double(), w)
+    np.testing.assert_allclose(single[:140], u.cpu().numpy().reshape(-1), rtol=1e-10, atol=1e-12)
+
+
+def test_degenerate_rotation_raises(pk):
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.errors import DegenerateRotation
+    from paper_2512_22575_b200.geometry import RigidTransform, Rotation3
+
+    chain, model = config.robot_7dof()
+    ee = robot.forward_kinematics(chain, np.zeros(7))[-1]
+    goal = RigidTransform(ee.rotation @ Rotation3.rot_x(math.pi), ee.translation)
+    params = config.planner_params(7, {"samples": 8, "horizon": 3, "sigma": 0.0})
+    for prec in ("fp32", "fp64"):
+        pl = planner.Planner(chain, model, params, prec)
+        with pytest.raises(DegenerateRotation):
+            pl.smpc_step(robot.JointState.resting(np.zeros(7)), goal, None, None, 0)
+
+
+def test_sampler_statistics(pk):
+    """Statistical parity with the reference sampler (t/test_planner.py:52-90)."""
+    pkg, config, mapping, planner, robot = pk
+    chain, model = config.robot_7dof()
+    params = config.planner_params(7, {"samples": 32, "horizon": 10})
+    eps = planner.sample_perturbations(params, 9).cpu().numpy()
+    np.testing.assert_array_equal(eps[0], 0.0)
+    assert np.abs(eps[1:]).max() > 0
+    a = planner.sample_perturbations(params, 1).cpu().numpy()
+    b = planner.sample_perturbations(params, 1).cpu().numpy()
+    c = planner.sample_perturbations(params, 2).cpu().numpy()
+    np.testing.assert_array_equal(a, b)
+    assert np.abs(a - c).max() > 0
+    # mean within 4 sigma / sqrt(M); smoothing preserves the variance (5%)
+    p2 = config.planner_params(7, {"samples": 100_000, "horizon": 2, "sigma": 2.0})
+    e2 = planner.sample_perturbations(p2, 123).cpu().numpy()
+    assert np.abs(e2.mean(axis=0)).max() < 4.0 * 2.0 / math.sqrt(100_000)
+    p3 = config.planner_params(7, {"samples": 20_000, "horizon": 12, "sigma": 1.5, "noise_window": 5})
+    e3 = planner.sample_perturbations(p3, 7).cpu().numpy()
+    np.testing.assert_allclose(e3[1:].std(axis=0), 1.5, rtol=0.05)
+    p4 = config.planner_params(7, {"samples": 16, "horizon": 8, "sigma": 0.0})
+    np.testing.assert_array_equal(planner.sample_perturbations(p4, 4).cpu().numpy(), 0.0)
+    # shard offsets reproduce the same global stream
+    pl = planner.Planner(chain, model, params, "fp64")
+    full = pl.sample_device(5)
+    half = pl.sample_device(5, m_offset=16, samples=16)
+    torch.testing.assert_close(full[16:], half, rtol=0, atol=0)
+
+
+def test_fixed_point_at_goal(pk):
+    """t/test_planner.py:420-430 on the 7-DoF arm: zero noise at the goal
+    keeps the command at zero."""
+    pkg, config, mapping, planner, robot = pk
+    chain, model = config.robot_7dof()
+    q = np.full(7, 0.4)
+    goal = robot.forward_kinematics(chain, q)[-1]
+    params = config.planner_params(7, {"sigma": 0.0, "samples": 16, "horizon": 10, "q_ref": q})
+    for prec in ("fp64", "fp32"):
+        res = planner.Planner(chain, model, params, prec).smpc_step(robot.JointState.resting(q), goal, None, None, 0)
+        np.testing.assert_allclose(res.command, 0.0, atol=1e-9)
+        np.testing.assert_allclose(res.next_nominal, 0.0, atol=1e-9)
