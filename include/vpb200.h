@@ -173,7 +173,8 @@ typedef struct {
 /* Rollout + cost evaluation of M control sequences.
  * Replaces vp/batch.py:161-336 (evaluate_batch, 49 args).
  * controls (dev) M x H x n of `dtype`; `nominal` (dev, H x n, same dtype) is
- * added to every sample when non-NULL (controls then hold perturbations).
+ * added to every sample when non-NULL (controls then hold perturbations);
+ * nominal is always f64, controls may be f32 or f64.
  * costs (dev) M f64, terms (dev) M x 6 f64, flags (dev) M u8 (1 = log-map
  * singularity, cost = inf); traj_q/traj_qd (dev, M x (H+1) x n f64) and
  * sphere_pos (dev, M x H x S x 3 f64) are optional (NULL = not stored). */
@@ -205,15 +206,16 @@ int vpb_update_controls(const double *nominal, const void *eps, int dtype,
  *   partials (local min m_c, Z_c = sum exp(-(S-m_c)/lam), N_c = sum w eps)
  *   merged in fixed order into this shard's partial
  *   part_out (dev) = [m_r, Z_r, N_r[H*n], count_nonfinite, best_index].
+ * m_offset = global index of local sample 0 (reported best_index).
  * The shard partial is what ranks exchange; a single
  * device calls vpb_smpc_finish directly on its own partial. */
 size_t vpb_smpc_workspace_bytes(int64_t M, int64_t H, int64_t n);
 int64_t vpb_smpc_partial_len(int64_t H, int64_t n);
 int vpb_smpc_partial(const vpb_problem *prob, const vpb_field *field,
                      const void *eps, int dtype, const double *nominal,
-                     int64_t M, int precision, double *costs, uint8_t *flags,
-                     double *part_out, void *workspace, size_t workspace_bytes,
-                     void *stream);
+                     int64_t M, int64_t m_offset, int precision,
+                     double *costs, uint8_t *flags, double *part_out,
+                     void *workspace, size_t workspace_bytes, void *stream);
 
 /* Merge R shard partials (R x partial_len, dev, fixed rank order) and finish
  * the step: U* = nominal + N/Z, then re-evaluate U* (M = 1) for the

@@ -101,7 +101,7 @@ SIGNATURES = {
     "vpb_update_controls": (ctypes.c_int, [_p, _p, ctypes.c_int, _p, _i64, _i64, _p, _p, _sz, _p]),
     "vpb_smpc_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "vpb_smpc_partial_len": (_i64, [_i64, _i64]),
-    "vpb_smpc_partial": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _p, ctypes.c_int, _p, _i64,
+    "vpb_smpc_partial": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _p, ctypes.c_int, _p, _i64, _i64,
                                         ctypes.c_int, _p, _p, _p, _p, _sz, _p]),
     "vpb_smpc_out_len": (_i64, [_i64, _i64]),
     "vpb_smpc_finish_workspace_bytes": (_sz, [_i64, _i64, _i64]),

@@ -68,6 +68,7 @@ struct RolloutIO {
   double *traj_q, *traj_qd, *sph_out;  // optional
   double *parts;           // per-CTA softmin partials (kPartHead + H n) or null
   double lam;
+  int64_t m_offset;        // global index of local sample 0 (best_index)
 };
 
 template <typename T, typename ET, int MAXJ>
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 2) rollout_kernel(const __grid_const
     part[0] = mn;
     part[1] = Z;
     part[2] = (double)nonfinite;
-    part[3] = best >= 0 ? (double)(cta_m0 + best) : -1.0;
+    part[3] = best >= 0 ? (double)(io.m_offset + cta_m0 + best) : -1.0;
   }
   for (int e = threadIdx.x; e < hn; e += blockDim.x) {
     double acc = 0.0;
@@ -735,7 +736,6 @@ int vpb_evaluate_batch(const vpb_problem *prob, const vpb_field *field, const vo
   VPB_REQUIRE(prob && controls && costs && flags, "null argument to vpb_evaluate_batch");
   VPB_REQUIRE(M >= 0, "M must be >= 0");
   VPB_REQUIRE((traj_q == nullptr) == (traj_qd == nullptr), "traj_q and traj_qd must both be given or both null");
-  VPB_REQUIRE(nominal == nullptr || dtype == VPB_DTYPE_F64, "nominal must be f64");
   RolloutIO io;
   memset(&io, 0, sizeof(io));
   io.ctrl = controls;
@@ -814,8 +814,8 @@ size_t vpb_smpc_workspace_bytes(int64_t M, int64_t H, int64_t n) {
 }
 
 int vpb_smpc_partial(const vpb_problem *prob, const vpb_field *field, const void *eps, int dtype,
-                     const double *nominal, int64_t M, int precision, double *costs, uint8_t *flags,
-                     double *part_out, void *workspace, size_t workspace_bytes, void *stream) {
+                     const double *nominal, int64_t M, int64_t m_offset, int precision, double *costs,
+                     uint8_t *flags, double *part_out, void *workspace, size_t workspace_bytes, void *stream) {
   VPB_REQUIRE(prob && eps && nominal && costs && flags && part_out && M >= 1, "bad arguments to vpb_smpc_partial");
   VPB_REQUIRE(prob->lam > 0.0, "temperature must be positive");
   const int64_t H = prob->horizon, n = prob->n_joints;
@@ -837,6 +837,7 @@ int vpb_smpc_partial(const vpb_problem *prob, const vpb_field *field, const void
   io.flags = flags;
   io.parts = parts;
   io.lam = prob->lam;
+  io.m_offset = m_offset;
   int rc = launch_rollout(prob, field, precision, dtype, io, s);
   if (rc) return rc;
   return merge_all(parts, ctas, H * n, prob->lam, tmp_a, tmp_b, part_out, s);

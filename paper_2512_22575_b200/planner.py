@@ -311,7 +311,8 @@ class Planner:
             D.stream(self.device)), "sample_perturbations")
         return out
 
-    def smpc_partial_device(self, state, goal, snap, nominal_dev: torch.Tensor, eps_dev: torch.Tensor):
+    def smpc_partial_device(self, state, goal, snap, nominal_dev: torch.Tensor, eps_dev: torch.Tensor,
+                            m_offset: int = 0):
         """Rollout + this shard's softmin partial (device, no sync).
         Returns (partial (L,) f64, costs (M,), flags (M,))."""
         m, h, n = eps_dev.shape
@@ -324,7 +325,8 @@ class Planner:
         ws_bytes = int(L.vpb_smpc_workspace_bytes(m, h, n))
         ws = D.Workspace.get(self.device, "smpc", ws_bytes)
         dtype = DTYPE_F32 if eps_dev.dtype == torch.float32 else DTYPE_F64
-        check(L.vpb_smpc_partial(P, _field_struct(snap), D.ptr(eps_dev), dtype, D.ptr(nominal_dev), m, self._prec,
+        check(L.vpb_smpc_partial(P, _field_struct(snap), D.ptr(eps_dev), dtype, D.ptr(nominal_dev), m, int(m_offset),
+                                 self._prec,
                                  D.ptr(costs), D.ptr(flags), D.ptr(part), D.ptr(ws), ws.numel(),
                                  D.stream(self.device)), "smpc_partial")
         return part, costs, flags

@@ -248,7 +248,8 @@ def test_smpc_shard_merge_equals_single(pk):
         parts = []
         step = 1024 // shards
         for r in range(shards):
-            p, c, _ = pl.smpc_partial_device(state, goal, None, nom, eps[r * step:(r + 1) * step].contiguous())
+            p, c, _ = pl.smpc_partial_device(state, goal, None, nom, eps[r * step:(r + 1) * step].contiguous(),
+                                              m_offset=r * step)
             torch.testing.assert_close(c, costs[r * step:(r + 1) * step], rtol=0, atol=0)
             parts.append(p)
         merged = pl.smpc_finish_device(state, goal, None, nom, torch.stack(parts)).cpu().numpy()
