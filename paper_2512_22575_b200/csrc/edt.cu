@@ -245,6 +245,200 @@ __global__ void __launch_bounds__(64) edt_pass_fh(const TIn *__restrict__ in, TO
 #undef STK
 }
 
+// ---------------------------------------------------------------------------
+// Fast z pass (box z-length <= 1024): one warp per (x, y) line.  Lane i holds
+// the i-th 32-bit word of the line's occupancy; a warp max-scan / min-scan
+// over the words gives every word the last source before it and the first
+// source after it, so each output needs one word and two shuffled carries.
+// Writes u16 nearest-source distances (0xFFFF = no source on the line).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) edt_pass_z_scan(const uint32_t *__restrict__ bits, int64_t gy,
+                                                       int64_t words_z, int64_t lo0, int64_t lo1, int lo2,
+                                                       int64_t n0, int64_t n1, int n2, uint16_t *__restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t line = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (line >= n0 * n1) return;
+  const int64_t i0 = line / n1, i1 = line - i0 * n1;
+  const uint32_t *w = bits + ((lo0 + i0) * gy + (lo1 + i1)) * words_z;
+  const int nw = (n2 + 31) >> 5;
+  uint32_t word = 0;
+  if (lane < nw) {
+    const int zb = lo2 + 32 * lane;  // global z of bit 0 of this window
+    const int wi = zb >> 5, sh = zb & 31;
+    const uint32_t a = __ldg(w + wi);
+    const uint32_t b = (sh != 0 && wi + 1 < words_z) ? __ldg(w + wi + 1) : 0u;
+    word = sh ? __funnelshift_r(a, b, sh) : a;
+    const int valid = n2 - 32 * lane;
+    if (valid < 32) word &= (1u << valid) - 1u;
+  }
+  // last source at or before each word / first source at or after it
+  int last = word ? 32 * lane + 31 - __clz(word) : -1;
+  int first = word ? 32 * lane + __ffs(word) - 1 : 0x7fffffff;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int l = __shfl_up_sync(kFull, last, d);
+    if (lane >= d) last = max(last, l);
+    const int f = __shfl_down_sync(kFull, first, d);
+    if (lane + d < 32) first = min(first, f);
+  }
+  // exclusive versions: before word i / after word i
+  int last_ex = __shfl_up_sync(kFull, last, 1);
+  if (lane == 0) last_ex = -1;
+  int first_ex = __shfl_down_sync(kFull, first, 1);
+  if (lane == 31) first_ex = 0x7fffffff;
+  uint16_t *o = out + line * n2;
+  const uint32_t le_mask = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+  const uint32_t ge_mask = 0xffffffffu << lane;
+  for (int c = 0; c < nw; ++c) {
+    const uint32_t wc = __shfl_sync(kFull, word, c);
+    const int lx = __shfl_sync(kFull, last_ex, c);
+    const int fx = __shfl_sync(kFull, first_ex, c);
+    const int z = 32 * c + lane;
+    const uint32_t le = wc & le_mask, ge = wc & ge_mask;
+    const int left = le ? 32 * c + 31 - __clz(le) : lx;
+    const int right = ge ? 32 * c + __ffs(ge) - 1 : fx;
+    int d = 0x7fffffff;
+    if (left >= 0) d = z - left;
+    if (right != 0x7fffffff) d = min(d, right - z);
+    if (z < n2) o[z] = d == 0x7fffffff ? kNoSrc16 : (uint16_t)min(d, 0xFFFE);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Shared-memory FH pass.  A 32-thread CTA owns 32 lines (lanes over the
+// contiguous z axis), stages them as a [len][32] u32 tile (coalesced loads,
+// conflict-free column access), runs the lower-envelope sweep per lane and
+// keeps its stack IN PLACE: stack entry k (packed (f << 10) | v) overwrites
+// tile slot k, whose input has always been consumed already (k <= q).  The
+// output sweep reads the stack and writes the line back coalesced.
+// len <= 1024 and f < 2^22 (3 (len-1)^2) so an entry fits 32 bits.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kTileInf = 0xFFFFFFFFu;
+
+template <typename TIn>
+__device__ __forceinline__ uint32_t tile_in(TIn v);
+template <>
+__device__ __forceinline__ uint32_t tile_in<uint16_t>(uint16_t d) {
+  return d == kNoSrc16 ? kTileInf : (uint32_t)d * (uint32_t)d;
+}
+template <>
+__device__ __forceinline__ uint32_t tile_in<int32_t>(int32_t v) {
+  return v == kNoSrc32 ? kTileInf : (uint32_t)v;
+}
+
+template <typename TOut>
+__device__ __forceinline__ void store_tile_out(TOut *p, uint32_t v);
+template <>
+__device__ __forceinline__ void store_tile_out<int32_t>(int32_t *p, uint32_t v) {
+  *p = v == kTileInf ? kNoSrc32 : (int32_t)v;
+}
+template <>
+__device__ __forceinline__ void store_tile_out<float>(float *p, uint32_t v) {
+  *p = v == kTileInf ? __int_as_float(0x7f800000) : (float)v;
+}
+
+template <typename TIn, typename TOut>
+__global__ void __launch_bounds__(32) edt_pass_fh_smem(const TIn *__restrict__ in, TOut *__restrict__ out,
+                                                       int64_t n_outer, int64_t outer_stride, int n2, int len,
+                                                       int64_t stride) {
+  extern __shared__ uint32_t tile[];  // [len][32]
+  const int lane = threadIdx.x;
+  const int zchunks = (n2 + 31) >> 5;
+  const int64_t a = blockIdx.x / zchunks;
+  const int z = (int)(blockIdx.x - a * zchunks) * 32 + lane;
+  if (a >= n_outer) return;
+  const bool act = z < n2;
+  const int64_t base = a * outer_stride + (act ? z : 0);
+  const TIn *src = in + base;
+  // ---- stage the 32 lines (8 independent loads in flight per thread) ----
+  int q = 0;
+  for (; q + 8 <= len; q += 8) {
+    TIn v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = act ? src[(int64_t)(q + t) * stride] : (TIn)0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) tile[(q + t) * 32 + lane] = act ? tile_in<TIn>(v[t]) : kTileInf;
+  }
+  for (; q < len; ++q) tile[q * 32 + lane] = act ? tile_in<TIn>(src[(int64_t)q * stride]) : kTileInf;
+  if (!act) return;
+  // ---- forward sweep: lower envelope, stack in place ----
+  int k = -1;
+  int vt = 0, vp = 0;
+  int Ft = 0, Fp = 0;
+  for (int qq = 0; qq < len; ++qq) {
+    const uint32_t e = tile[qq * 32 + lane];
+    if (e == kTileInf) continue;
+    const int fq = (int)e;
+    const int Fq = fq + qq * qq;
+    while (k >= 1) {
+      // pop the top if s(vt, q) <= s(vp, vt)
+      if ((long long)(Fq - Ft) * (vt - vp) <= (long long)(Ft - Fp) * (qq - vt)) {
+        --k;
+        vt = vp;
+        Ft = Fp;
+        if (k >= 1) {
+          const uint32_t se = tile[(k - 1) * 32 + lane];
+          vp = (int)(se & 1023u);
+          Fp = (int)(se >> 10) + vp * vp;
+        }
+      } else {
+        break;
+      }
+    }
+    ++k;
+    tile[k * 32 + lane] = ((uint32_t)fq << 10) | (uint32_t)qq;
+    vp = vt;
+    Fp = Ft;
+    vt = qq;
+    Ft = Fq;
+  }
+  TOut *dst = out + base;
+  if (k < 0) {
+    for (int qq = 0; qq < len; ++qq) store_tile_out<TOut>(dst + (int64_t)qq * stride, kTileInf);
+    return;
+  }
+  // ---- output sweep ----
+  int j = 0;
+  uint32_t se = tile[lane];
+  int vj = (int)(se & 1023u), fj = (int)(se >> 10);
+  int Fj = fj + vj * vj;
+  int vn = 0, fn = 0, Fn = 0;
+  if (k >= 1) {
+    se = tile[32 + lane];
+    vn = (int)(se & 1023u);
+    fn = (int)(se >> 10);
+    Fn = fn + vn * vn;
+  }
+  for (int qq = 0; qq < len; ++qq) {
+    while (j < k && (Fn - Fj) < 2 * qq * (vn - vj)) {
+      ++j;
+      vj = vn;
+      fj = fn;
+      Fj = Fn;
+      if (j < k) {
+        se = tile[(j + 1) * 32 + lane];
+        vn = (int)(se & 1023u);
+        fn = (int)(se >> 10);
+        Fn = fn + vn * vn;
+      }
+    }
+    const int dq = qq - vj;
+    store_tile_out<TOut>(dst + (int64_t)qq * stride, (uint32_t)(dq * dq + fj));
+  }
+}
+
+template <typename TIn, typename TOut>
+static int launch_fh_smem(const TIn *in, TOut *out, int64_t n_outer, int64_t outer_stride, int64_t n2, int64_t len,
+                          int64_t stride, cudaStream_t s) {
+  const int64_t blocks = n_outer * ((n2 + 31) >> 5);
+  if (blocks == 0) return VPB_OK;
+  const size_t smem = (size_t)len * 32 * sizeof(uint32_t);
+  auto kern = edt_pass_fh_smem<TIn, TOut>;
+  if (smem > 48 * 1024) VPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<(unsigned)blocks, 32, smem, s>>>(in, out, n_outer, outer_stride, (int)n2, (int)len, stride);
+  return check_launch("edt_pass_fh_smem");
+}
+
 template <typename TIn, typename TOut>
 static int launch_fh(const TIn *in, TOut *out, int64_t n_outer, int64_t outer_stride, int64_t n2, int64_t len,
                      int64_t stride, int64_t max_dim, cudaStream_t s) {
@@ -293,8 +487,14 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], dou
   const int64_t lines_z = n[0] * n[1];
   if (use_bits) {
     VPB_REQUIRE(grid->occ_bits, "use_bits set but grid->occ_bits is null");
-    edt_pass_z_bits<<<(unsigned)ceil_div(lines_z, 8), 256, 0, s>>>(
-        grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], lo[2], n[0], n[1], n[2], dz);
+    if (n[2] <= 1024) {
+      edt_pass_z_scan<<<(unsigned)ceil_div(lines_z, 8), 256, 0, s>>>(grid->occ_bits, grid->dims[1],
+                                                                     ceil_div(grid->dims[2], 32), lo[0], lo[1],
+                                                                     (int)lo[2], n[0], n[1], (int)n[2], dz);
+    } else {
+      edt_pass_z_bits<<<(unsigned)ceil_div(lines_z, 8), 256, 0, s>>>(
+          grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], lo[2], n[0], n[1], n[2], dz);
+    }
   } else {
     VPB_REQUIRE(grid->log_odds, "log_odds is null");
     edt_pass_z_logodds<<<(unsigned)ceil_div(lines_z, 8), 256, 0, s>>>(
@@ -303,10 +503,15 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], dou
   int rc = check_launch("edt_pass_z");
   if (rc) return rc;
   const int64_t maxd = n[0] > n[1] ? (n[0] > n[2] ? n[0] : n[2]) : (n[1] > n[2] ? n[1] : n[2]);
-  // Pass Y: lines (x, z), element y at stride n2, outer stride n1*n2.
+  if (maxd <= 1024) {
+    // Pass Y: lines (x, z), element y at stride n2, outer stride n1*n2.
+    rc = launch_fh_smem<uint16_t, int32_t>(dz, g2, n[0], n[1] * n[2], n[2], n[1], n[2], s);
+    if (rc) return rc;
+    // Pass X: lines (y, z), element x at stride n1*n2, outer stride n2.
+    return launch_fh_smem<int32_t, float>(g2, out_sq, n[1], n[2], n[2], n[0], n[1] * n[2], s);
+  }
   rc = launch_fh<uint16_t, int32_t>(dz, g2, n[0], n[1] * n[2], n[2], n[1], n[2], maxd, s);
   if (rc) return rc;
-  // Pass X: lines (y, z), element x at stride n1*n2, outer stride n2.
   return launch_fh<int32_t, float>(g2, out_sq, n[1], n[2], n[2], n[0], n[1] * n[2], maxd, s);
 }
 

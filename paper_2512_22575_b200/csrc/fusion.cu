@@ -33,6 +33,9 @@ struct FusionArgs {
   double tau, l_hit, l_miss, l_min, l_max, l_thr;
   int n_mask;
   double aabb_lo[3], aabb_hi[3];
+  // fp32 prefilter constants
+  float of0, of1, of2, oabs, voxf, rf[9], tf[3], tabs, fxf, fyf, cxf, cyf, wf, hf;
+  float bb_lo[3], bb_hi[3];
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr2[VPB_MAX_MASK_SPHERES];
 };
@@ -61,61 +64,112 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
   double newval = 0.0;
 
   if (in_box) {
-    // Voxel centre: origin + (i + 0.5) * voxel  (vp/mapping.py:306-308)
-    const double px = dadd(A.origin0, dmul(dadd((double)x, 0.5), A.voxel));
-    const double py = dadd(A.origin1, dmul(dadd((double)y, 0.5), A.voxel));
-    const double pz = dadd(A.origin2, dmul(dadd((double)z, 0.5), A.voxel));
-
-    // Robot mask (vp/mapping.py:310-325).  Conservative AABB pre-reject:
-    // the box is padded by 1e-9 m on the host so rounding in the bounds can
-    // never reject a voxel the exact strict-< test would accept.
-    bool masked = false;
-    if (A.n_mask > 0 && px >= A.aabb_lo[0] && px <= A.aabb_hi[0] && py >= A.aabb_lo[1] &&
-        py <= A.aabb_hi[1] && pz >= A.aabb_lo[2] && pz <= A.aabb_hi[2]) {
-      for (int s = 0; s < A.n_mask; ++s) {
-        const double dx = dsub(px, A.mc[3 * s + 0]);
-        const double dy = dsub(py, A.mc[3 * s + 1]);
-        const double dz = dsub(pz, A.mc[3 * s + 2]);
-        const double d2 = dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
-        if (d2 < A.mr2[s]) {
-          masked = true;
-          break;
+    // ---- conservative fp32 prefilter ---------------------------------------
+    // Decides, with explicit error bounds, the voxels whose reference result
+    // is certainly "skip" (behind the camera, outside the image, or landing on
+    // a pixel without a usable return).  Everything else -- robot-mask
+    // candidates, pixel-boundary ambiguities, voxels that fuse -- takes the
+    // exact fp64 path below, so the result is bitwise the reference's.
+    const float axf = ((float)x + 0.5f) * A.voxf, ayf = ((float)y + 0.5f) * A.voxf, azf = ((float)z + 0.5f) * A.voxf;
+    const float pxf = A.of0 + axf;
+    const float pyf = A.of1 + ayf;
+    const float pzf = A.of2 + azf;
+    bool exact = false;
+    if (A.n_mask > 0 && pxf >= A.bb_lo[0] && pxf <= A.bb_hi[0] && pyf >= A.bb_lo[1] && pyf <= A.bb_hi[1] &&
+        pzf >= A.bb_lo[2] && pzf <= A.bb_hi[2])
+      exact = true;  // possibly inside a mask sphere
+    if (!exact) {
+      const float qxf = fmaf(A.rf[0], pxf, fmaf(A.rf[1], pyf, fmaf(A.rf[2], pzf, A.tf[0])));
+      const float qyf = fmaf(A.rf[3], pxf, fmaf(A.rf[4], pyf, fmaf(A.rf[5], pzf, A.tf[1])));
+      const float qzf = fmaf(A.rf[6], pxf, fmaf(A.rf[7], pyf, fmaf(A.rf[8], pzf, A.tf[2])));
+      // |q_f - q| <= dq: each centre coordinate is off by <= 2e-7 (|origin| +
+      // |(i + 1/2) voxel|) (no cancellation assumed), rotation entries are <= 1
+      // and the three FMAs add <= 2e-7 of the row magnitude: 4e-7 in total,
+      // taken with a 2.5x margin.
+      const float dq = 1e-6f * (A.oabs + fabsf(axf) + fabsf(ayf) + fabsf(azf) + A.tabs) + 1e-12f;
+      if (qzf < -dq) {
+        // qz <= 0 for sure: the reference skips this voxel
+      } else if (qzf <= dq + 1e-30f) {
+        exact = true;
+      } else {
+        const float iz = 1.0f / qzf;
+        const float ue = fmaf(A.fxf * qxf, iz, A.cxf) + 0.5f;
+        const float ve = fmaf(A.fyf * qyf, iz, A.cyf) + 0.5f;
+        const float den = qzf * (qzf - dq);
+        const float du = 2.0f * A.fxf * dq * (fabsf(qxf) + qzf) / den + 1e-6f * (fabsf(ue) + fabsf(A.cxf)) + 1e-5f;
+        const float dv = 2.0f * A.fyf * dq * (fabsf(qyf) + qzf) / den + 1e-6f * (fabsf(ve) + fabsf(A.cyf)) + 1e-5f;
+        const bool out_u = (ue < -du) || (ue >= A.wf + du);
+        const bool out_v = (ve < -dv) || (ve >= A.hf + dv);
+        if (!(out_u || out_v)) {
+          const float fu = floorf(ue), fv = floorf(ve);
+          const bool amb = (ue - fu <= du) || (fu + 1.0f - ue <= du) || (ve - fv <= dv) || (fv + 1.0f - ve <= dv) ||
+                           fu < 0.0f || fu >= A.wf || fv < 0.0f || fv >= A.hf;
+          if (amb) {
+            exact = true;
+          } else {
+            const int64_t pix = (int64_t)fv * A.width + (int64_t)fu;
+            const double measured = __ldg(A.depth + pix);
+            exact = measured >= A.d_min && measured <= A.d_max && !__ldg(A.pixel_masked + pix);
+          }
         }
+        // else: certainly outside the image -> skip
       }
     }
-    if (masked) {
-      const double old = A.log_odds[g];
-      newval = old > 0.0 ? 0.0 : old;
-      if (old > 0.0) A.log_odds[g] = 0.0;
-      A.observed[g] = 1;
-      touched = true;
-    } else {
-      // Camera transform (vp/mapping.py:327-329): ((r0 px + r1 py) + r2 pz) + t
-      const double qx = dadd(dadd(dadd(dmul(A.r[0], px), dmul(A.r[1], py)), dmul(A.r[2], pz)), A.t[0]);
-      const double qy = dadd(dadd(dadd(dmul(A.r[3], px), dmul(A.r[4], py)), dmul(A.r[5], pz)), A.t[1]);
-      const double qz = dadd(dadd(dadd(dmul(A.r[6], px), dmul(A.r[7], py)), dmul(A.r[8], pz)), A.t[2]);
-      if (qz > 0.0) {
-        // u = fx * qx / qz + cx ; nearest pixel floor(u + 0.5) (:332-335)
-        const double u = dadd(__ddiv_rn(dmul(A.fx, qx), qz), A.cx);
-        const double v = dadd(__ddiv_rn(dmul(A.fy, qy), qz), A.cy);
-        const double uf = floor(dadd(u, 0.5));
-        const double vf = floor(dadd(v, 0.5));
-        if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
-          const int64_t pix = (int64_t)vf * A.width + (int64_t)uf;
-          const double measured = __ldg(A.depth + pix);
-          if (measured >= A.d_min && measured <= A.d_max && !__ldg(A.pixel_masked + pix)) {
-            const double diff = dsub(qz, measured);
-            int cls = 0;
-            if (fabs(diff) <= A.tau) cls = 1;                    // hit
-            else if (qz < dsub(measured, A.tau)) cls = 2;        // miss
-            if (cls) {
-              double value = dadd(A.log_odds[g], cls == 1 ? A.l_hit : A.l_miss);
-              if (value < A.l_min) value = A.l_min;
-              else if (value > A.l_max) value = A.l_max;
-              A.log_odds[g] = value;
-              A.observed[g] = 1;
-              newval = value;
-              touched = true;
+
+    if (exact) {
+      // ---- exact fp64 path: the reference's operations in its order ------
+      const double px = dadd(A.origin0, dmul(dadd((double)x, 0.5), A.voxel));
+      const double py = dadd(A.origin1, dmul(dadd((double)y, 0.5), A.voxel));
+      const double pz = dadd(A.origin2, dmul(dadd((double)z, 0.5), A.voxel));
+      // Robot mask (vp/mapping.py:310-325), exact strict-< test.
+      bool masked = false;
+      if (A.n_mask > 0 && px >= A.aabb_lo[0] && px <= A.aabb_hi[0] && py >= A.aabb_lo[1] &&
+          py <= A.aabb_hi[1] && pz >= A.aabb_lo[2] && pz <= A.aabb_hi[2]) {
+        for (int s = 0; s < A.n_mask; ++s) {
+          const double dx = dsub(px, A.mc[3 * s + 0]);
+          const double dy = dsub(py, A.mc[3 * s + 1]);
+          const double dz = dsub(pz, A.mc[3 * s + 2]);
+          const double d2 = dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
+          if (d2 < A.mr2[s]) {
+            masked = true;
+            break;
+          }
+        }
+      }
+      if (masked) {
+        const double old = A.log_odds[g];
+        newval = old > 0.0 ? 0.0 : old;
+        if (old > 0.0) A.log_odds[g] = 0.0;
+        A.observed[g] = 1;
+        touched = true;
+      } else {
+        // Camera transform (vp/mapping.py:327-329): ((r0 px + r1 py) + r2 pz) + t
+        const double qx = dadd(dadd(dadd(dmul(A.r[0], px), dmul(A.r[1], py)), dmul(A.r[2], pz)), A.t[0]);
+        const double qy = dadd(dadd(dadd(dmul(A.r[3], px), dmul(A.r[4], py)), dmul(A.r[5], pz)), A.t[1]);
+        const double qz = dadd(dadd(dadd(dmul(A.r[6], px), dmul(A.r[7], py)), dmul(A.r[8], pz)), A.t[2]);
+        if (qz > 0.0) {
+          // u = fx * qx / qz + cx ; nearest pixel floor(u + 0.5) (:332-335)
+          const double u = dadd(__ddiv_rn(dmul(A.fx, qx), qz), A.cx);
+          const double v = dadd(__ddiv_rn(dmul(A.fy, qy), qz), A.cy);
+          const double uf = floor(dadd(u, 0.5));
+          const double vf = floor(dadd(v, 0.5));
+          if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
+            const int64_t pix = (int64_t)vf * A.width + (int64_t)uf;
+            const double measured = __ldg(A.depth + pix);
+            if (measured >= A.d_min && measured <= A.d_max && !__ldg(A.pixel_masked + pix)) {
+              const double diff = dsub(qz, measured);
+              int cls = 0;
+              if (fabs(diff) <= A.tau) cls = 1;                    // hit
+              else if (qz < dsub(measured, A.tau)) cls = 2;        // miss
+              if (cls) {
+                double value = dadd(A.log_odds[g], cls == 1 ? A.l_hit : A.l_miss);
+                if (value < A.l_min) value = A.l_min;
+                else if (value > A.l_max) value = A.l_max;
+                A.log_odds[g] = value;
+                A.observed[g] = 1;
+                newval = value;
+                touched = true;
+              }
             }
           }
         }
@@ -285,6 +339,29 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3
   A.tau = p->tau; A.l_hit = p->l_hit; A.l_miss = p->l_miss;
   A.l_min = p->l_min; A.l_max = p->l_max; A.l_thr = p->l_occ_threshold;
   A.n_mask = (int)n_mask;
+  A.of0 = (float)A.origin0;
+  A.of1 = (float)A.origin1;
+  A.of2 = (float)A.origin2;
+  A.voxf = (float)A.voxel;
+  A.oabs = fabsf(A.of0) + fabsf(A.of1) + fabsf(A.of2);
+  A.tabs = 0.0f;
+  for (int k = 0; k < 9; ++k) A.rf[k] = (float)A.r[k];
+  for (int k = 0; k < 3; ++k) {
+    A.tf[k] = (float)A.t[k];
+    A.tabs += fabsf(A.tf[k]);
+    // fp32 AABB of the mask spheres with a generous pad (fp32 centre error)
+    const double pad = 1e-4 + 1e-5 * (fabs(A.aabb_lo[k]) + fabs(A.aabb_hi[k]));
+    A.bb_lo[k] = (float)(A.aabb_lo[k] - pad);
+    A.bb_hi[k] = (float)(A.aabb_hi[k] + pad);
+  }
+  A.fxf = (float)A.fx;
+  A.fyf = (float)A.fy;
+  A.cxf = (float)A.cx;
+  A.cyf = (float)A.cy;
+  A.wf = (float)A.width;
+  A.hf = (float)A.height;
+  // the fp32 prefilter assumes an orthonormal world->camera rotation and a
+  // scene within float range; anything else simply takes the exact path
   const int64_t warps = A.n0 * A.n1 * A.wz_count;
   fuse_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, as_stream(stream)>>>(A);
   return check_launch("fuse_kernel");

@@ -158,14 +158,31 @@ __global__ void __launch_bounds__(kThreads, 2) rollout_kernel(const __grid_const
             }
           }
         }
-        // ---- FK with sphere centres emitted link by link ----
+        // limits / smoothness / null space first (vp/batch.py:303-311) so u
+        // and qd are dead before the FK
+        T lim = 0, sm = 0, nu = 0;
+#pragma unroll
+        for (int j = 0; j < MAXJ; ++j) {
+          if (j < nj) {
+            const T vq = bound_violation<T>(q[j], P.pos_lo[j], P.pos_hi[j]);
+            const T vv = bound_violation<T>(qd[j], P.vel_lo[j], P.vel_hi[j]);
+            const T va = bound_violation<T>(u[j], P.acc_lo[j], P.acc_hi[j]);
+            lim += P.w_q * vq * vq + P.w_qd * vv * vv + P.w_qdd * va * va;
+            sm += P.w_s * u[j] * u[j];
+            const T dq = q[j] - P.q_ref[j];
+            nu += P.w_ns * dq * dq;
+          }
+        }
+        s_lim += lim;
+        s_smooth += sm;
+        s_null += nu;
+        // ---- FK; sphere centres emitted link by link into shared memory ----
         T R[9], t[3];
 #pragma unroll
         for (int a = 0; a < 9; ++a) R[a] = P.base_r[a];
         t[0] = P.base_t[0];
         t[1] = P.base_t[1];
         t[2] = P.base_t[2];
-        T coll = T(0);
 #pragma unroll
         for (int li = 0; li <= MAXJ; ++li) {
           if (li > nj) break;
@@ -184,11 +201,6 @@ __global__ void __launch_bounds__(kThreads, 2) rollout_kernel(const __grid_const
               o[1] = (double)py;
               o[2] = (double)pz;
             }
-            if (P.has_field) {
-              const T dist = query_metric<T>(P, px, py, pz);
-              const T gap = P.d_act - (dist - P.sph_r[s]);
-              if (gap > T(0)) coll += P.w_env * gap * gap;
-            }
           }
         }
         T pc;
@@ -197,6 +209,26 @@ __global__ void __launch_bounds__(kThreads, 2) rollout_kernel(const __grid_const
           pc = T(0);
         }
         s_pose += pc;
+        T coll = T(0);
+        // environment term (vp/batch.py:250-293): two spheres per batch, all
+        // sixteen corner loads in flight before any is consumed
+        if (P.has_field) {
+          for (int s0 = 0; s0 < ns; s0 += 2) {
+            Query<T> Qa, Qb;
+            const bool hb = s0 + 1 < ns;
+            query_issue<T>(P, cen[(3 * s0) * 32], cen[(3 * s0 + 1) * 32], cen[(3 * s0 + 2) * 32], Qa);
+            const int s1 = hb ? s0 + 1 : s0;
+            query_issue<T>(P, cen[(3 * s1) * 32], cen[(3 * s1 + 1) * 32], cen[(3 * s1 + 2) * 32], Qb);
+            const T da = query_finish<T>(P, Qa);
+            const T ga = P.d_act - (da - P.sph_r[s0]);
+            if (ga > T(0)) coll += P.w_env * ga * ga;
+            if (hb) {
+              const T db = query_finish<T>(P, Qb);
+              const T gb = P.d_act - (db - P.sph_r[s1]);
+              if (gb > T(0)) coll += P.w_env * gb * gb;
+            }
+          }
+        }
         // self pairs (vp/batch.py:294-302)
         for (int p = 0; p < P.np; ++p) {
           const int i = P.pairs[2 * p], jj = P.pairs[2 * p + 1];
@@ -207,23 +239,6 @@ __global__ void __launch_bounds__(kThreads, 2) rollout_kernel(const __grid_const
           if (gap < T(0)) coll += P.w_self * gap * gap;
         }
         s_coll += coll;
-        // limits / smoothness / null space (vp/batch.py:303-311)
-        T lim = 0, sm = 0, nu = 0;
-#pragma unroll
-        for (int j = 0; j < MAXJ; ++j) {
-          if (j < nj) {
-            const T vq = bound_violation<T>(q[j], P.pos_lo[j], P.pos_hi[j]);
-            const T vv = bound_violation<T>(qd[j], P.vel_lo[j], P.vel_hi[j]);
-            const T va = bound_violation<T>(u[j], P.acc_lo[j], P.acc_hi[j]);
-            lim += P.w_q * vq * vq + P.w_qd * vv * vv + P.w_qdd * va * va;
-            sm += P.w_s * u[j] * u[j];
-            const T dq = q[j] - P.q_ref[j];
-            nu += P.w_ns * dq * dq;
-          }
-        }
-        s_lim += lim;
-        s_smooth += sm;
-        s_null += nu;
       }
     }
     // fixed-order warp reduction in fp64

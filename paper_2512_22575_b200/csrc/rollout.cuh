@@ -60,9 +60,23 @@ __device__ __forceinline__ void tsincos<float>(float x, float *s, float *c) { si
 template <>
 __device__ __forceinline__ void tsincos<double>(double x, double *s, double *c) { sincos(x, s, c); }
 
-// _query_metric, vp/mapping.py:616-685.
+// _query_metric, vp/mapping.py:616-685, split in two so a warp can issue the
+// eight corner loads of several spheres before consuming any of them.  The
+// reference first reads the containing cell (sq == 0 -> 0, inf -> inf); that
+// cell is always one of the eight interpolation corners (cell index
+// floor(g) is either floor(g - 1/2) or floor(g - 1/2) + 1, also at the clamped
+// borders), so it is selected from the loaded corners instead of being a
+// separate dependent load.
 template <typename T>
-__device__ __forceinline__ T query_metric(const Prob<T> &P, T px, T py, T pz) {
+struct Query {
+  T f0, f1, f2;
+  float v[8];
+  uint8_t cell;  // index of the containing cell among the corners
+  bool outside;
+};
+
+template <typename T>
+__device__ __forceinline__ void query_issue(const Prob<T> &P, T px, T py, T pz, Query<T> &Q) {
   T g0, g1, g2;
   if constexpr (sizeof(T) == 8) {
     g0 = (px - P.origin0) / P.voxel - P.lo0;
@@ -74,13 +88,11 @@ __device__ __forceinline__ T query_metric(const Prob<T> &P, T px, T py, T pz) {
     g2 = (pz - P.origin2) * P.inv_voxel - P.lo2;
   }
   const int n0 = P.n0, n1 = P.n1, n2 = P.n2;
-  if (!(g0 >= T(0) && g0 < T(n0) && g1 >= T(0) && g1 < T(n1) && g2 >= T(0) && g2 < T(n2)))
-    return P.outside;
+  Q.outside = !(g0 >= T(0) && g0 < T(n0) && g1 >= T(0) && g1 < T(n1) && g2 >= T(0) && g2 < T(n2));
+  if (Q.outside) {
+    g0 = g1 = g2 = T(0);
+  }
   const int i0 = (int)g0, i1 = (int)g1, i2 = (int)g2;
-  const float *sq = P.sq;
-  const float cell = __ldg(sq + ((size_t)i0 * n1 + i1) * n2 + i2);
-  if (cell == 0.0f) return T(0);
-  if (isinf(cell)) return cell;  // no source in the volume: all values inf
   T c0 = g0 - T(0.5), c1 = g1 - T(0.5), c2 = g2 - T(0.5);
   c0 = c0 < T(0) ? T(0) : (c0 > T(n0 - 1) ? T(n0 - 1) : c0);
   c1 = c1 < T(0) ? T(0) : (c1 > T(n1 - 1) ? T(n1 - 1) : c1);
@@ -89,21 +101,40 @@ __device__ __forceinline__ T query_metric(const Prob<T> &P, T px, T py, T pz) {
   const int b0 = a0 + 1 < n0 ? a0 + 1 : a0;
   const int b1 = a1 + 1 < n1 ? a1 + 1 : a1;
   const int b2 = a2 + 1 < n2 ? a2 + 1 : a2;
-  const T f0 = c0 - T(a0), f1 = c1 - T(a1), f2 = c2 - T(a2);
+  Q.f0 = c0 - T(a0);
+  Q.f1 = c1 - T(a1);
+  Q.f2 = c2 - T(a2);
+  Q.cell = (uint8_t)(((i0 == a0) ? 0 : 4) | ((i1 == a1) ? 0 : 2) | ((i2 == a2) ? 0 : 1));
+  const float *sq = P.sq;
   const size_t r00 = ((size_t)a0 * n1 + a1) * n2, r01 = ((size_t)a0 * n1 + b1) * n2;
   const size_t r10 = ((size_t)b0 * n1 + a1) * n2, r11 = ((size_t)b0 * n1 + b1) * n2;
-  const T v000 = (T)__ldg(sq + r00 + a2), v001 = (T)__ldg(sq + r00 + b2);
-  const T v010 = (T)__ldg(sq + r01 + a2), v011 = (T)__ldg(sq + r01 + b2);
-  const T v100 = (T)__ldg(sq + r10 + a2), v101 = (T)__ldg(sq + r10 + b2);
-  const T v110 = (T)__ldg(sq + r11 + a2), v111 = (T)__ldg(sq + r11 + b2);
-  const T e0 = T(1) - f0, e1 = T(1) - f1, e2 = T(1) - f2;
-  const T c00 = v000 * e0 + v100 * f0;
-  const T c01 = v001 * e0 + v101 * f0;
-  const T c10 = v010 * e0 + v110 * f0;
-  const T c11 = v011 * e0 + v111 * f0;
-  const T c0v = c00 * e1 + c10 * f1;
-  const T c1v = c01 * e1 + c11 * f1;
-  const T value = c0v * e2 + c1v * f2;
+  Q.v[0] = __ldg(sq + r00 + a2);
+  Q.v[1] = __ldg(sq + r00 + b2);
+  Q.v[2] = __ldg(sq + r01 + a2);
+  Q.v[3] = __ldg(sq + r01 + b2);
+  Q.v[4] = __ldg(sq + r10 + a2);
+  Q.v[5] = __ldg(sq + r10 + b2);
+  Q.v[6] = __ldg(sq + r11 + a2);
+  Q.v[7] = __ldg(sq + r11 + b2);
+}
+
+template <typename T>
+__device__ __forceinline__ T query_finish(const Prob<T> &P, const Query<T> &Q) {
+  if (Q.outside) return P.outside;
+  float cell = Q.v[0];
+#pragma unroll
+  for (int c = 1; c < 8; ++c)
+    if (Q.cell == c) cell = Q.v[c];
+  if (cell == 0.0f) return T(0);
+  if (isinf(cell)) return (T)cell;  // no source in the volume: all values inf
+  const T e0 = T(1) - Q.f0, e1 = T(1) - Q.f1, e2 = T(1) - Q.f2;
+  const T c00 = (T)Q.v[0] * e0 + (T)Q.v[4] * Q.f0;
+  const T c01 = (T)Q.v[1] * e0 + (T)Q.v[5] * Q.f0;
+  const T c10 = (T)Q.v[2] * e0 + (T)Q.v[6] * Q.f0;
+  const T c11 = (T)Q.v[3] * e0 + (T)Q.v[7] * Q.f0;
+  const T c0v = c00 * e1 + c10 * Q.f1;
+  const T c1v = c01 * e1 + c11 * Q.f1;
+  const T value = c0v * e2 + c1v * Q.f2;
   return P.voxel * tsqrt<T>(value);
 }
 
