@@ -256,3 +256,55 @@ def test_query_golden(M):
                                 torch.from_numpy(sq.astype(np.float32)).cuda(), outside)
         got = M.query_distances(field, g[f"q_pts_{i}"])
         np.testing.assert_array_equal(got, g[f"q_val_{i}"], err_msg=str(g[f"q_name_{i}"]))
+
+
+def _random_rotation(rng):
+    from paper_2512_22575_b200.geometry import Rotation3
+
+    q = rng.normal(size=4)
+    q /= np.linalg.norm(q)
+    w, x, y, z = q
+    m = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                  [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                  [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+    u, _, vt = np.linalg.svd(m)
+    return Rotation3(u @ vt)
+
+
+def test_fusion_prefilter_stress_vs_oracle(M):
+    """Arbitrary camera rotations/positions (inside and outside the grid),
+    plus a camera whose projections land exactly on pixel boundaries, so the
+    conservative fp32 prefilter's ambiguous branches are exercised."""
+    from paper_2512_22575_b200 import scene
+    from paper_2512_22575_b200.geometry import RigidTransform, Rotation3
+
+    rng = np.random.default_rng(314)
+    dims = (40, 33, 50)
+    grid = M.VoxelGrid((-0.4, -0.33, 0.0), 0.02, dims)
+    lo = np.zeros(dims)
+    ob = np.zeros(dims, bool)
+    cams = []
+    for _ in range(10):
+        pose = RigidTransform(_random_rotation(rng), rng.uniform(-1.5, 1.5, size=3))
+        cams.append(M.CameraModel(rng.uniform(40, 200), rng.uniform(40, 200), rng.uniform(10, 60),
+                                  rng.uniform(10, 50), 64, 48, 0.05, 20.0, pose=pose))
+    # boundary camera: unit focal length, voxel centres at x = k*0.02 + 0.01 project to
+    # u = x/z with z = 0.02 * odd -> exact half-integers appear
+    pose = RigidTransform(Rotation3.identity(), (0.4 - 0.01, 0.33 - 0.01, -0.01))
+    cams.append(M.CameraModel(1.0, 1.0, 0.0, 0.0, 64, 48, 0.001, 20.0, pose=pose))
+    for i, cam in enumerate(cams):
+        c = rng.uniform([-0.3, -0.3, 0.2], [0.3, 0.3, 0.9])
+        spheres = (np.array([[0.05, -0.02, 0.5], [-0.1, 0.1, 0.3]]), np.array([0.11, 0.07]))
+        d = scene.render_boxes(cam, [(c - 0.15, c + 0.15), ((-5, -5, 1.0), (5, 5, 1.1))], spheres)
+        if i == len(cams) - 1:
+            d = np.full((48, 64), 0.5)  # flat wall in front of the boundary camera
+        M.update_occupancy(grid, M.DepthImage(d), cam, mask=spheres)
+        pm = oracle.masked_pixels(d, cam.fx, cam.fy, cam.cx, cam.cy, cam.d_min, cam.d_max,
+                                  cam.pose.rotation.matrix, cam.pose.translation, spheres[0], spheres[1], 0.01)
+        r, t = cam.world_to_camera()
+        oracle.fuse_voxels(lo, ob, (0, 0, 0), dims, grid.origin, grid.voxel_size, r, t, cam.fx, cam.fy, cam.cx,
+                           cam.cy, cam.width, cam.height, cam.d_min, cam.d_max, d, pm, spheres[0], spheres[1],
+                           grid.tau, 0.85, -0.4, -2.0, 3.5)
+        np.testing.assert_array_equal(grid.log_odds_host(), lo, err_msg=f"camera {i}")
+        np.testing.assert_array_equal(grid.observed_host(), ob, err_msg=f"camera {i}")
+    assert ob.sum() > 1000
