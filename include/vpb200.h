@@ -162,6 +162,10 @@ typedef struct {
   double q0[VPB_MAX_JOINTS], qd0[VPB_MAX_JOINTS];
   double w_env, w_self, w_q, w_qd, w_qdd, w_s, w_ns, d_act;
   double lam; /* softmin temperature (vp/planner.py:373-384) */
+  /* (dev, optional) per-call state [q0 (n), qd0 (n), goal_r (9), goal_t (3)]
+   * f64; when set it overrides q0/qd0/goal_* so a captured CUDA graph can be
+   * replayed after one small host->device copy. */
+  const double *dyn_state;
 } vpb_problem;
 
 #define VPB_PREC_F32 0 /* production: fp32 arithmetic, fp64 cost sums */
@@ -200,15 +204,15 @@ int vpb_update_controls(const double *nominal, const void *eps, int dtype,
                         double *out, void *workspace, size_t workspace_bytes,
                         void *stream);
 
-/* One fused SMPC iteration on this device's shard of samples
- * (vp/planner.py:594-630 smpc_step minus sampling):
- *   rollout of nominal + eps (M local samples) -> costs; per-CTA softmin
- *   partials (local min m_c, Z_c = sum exp(-(S-m_c)/lam), N_c = sum w eps)
- *   merged in fixed order into this shard's partial
- *   part_out (dev) = [m_r, Z_r, N_r[H*n], count_nonfinite, best_index].
- * m_offset = global index of local sample 0 (reported best_index).
- * The shard partial is what ranks exchange; a single
- * device calls vpb_smpc_finish directly on its own partial. */
+/* One SMPC iteration on this device's shard of samples, in ONE kernel launch
+ * (vp/planner.py:594-630 smpc_step minus sampling): rollout of nominal + eps
+ * (M local samples, eps of `dtype`, nominal f64 H x n) -> per-CTA softmin
+ * partials (local min m_c, Z_c = sum exp(-(S-m_c)/lam), N_c = sum w eps) ->
+ * fixed-order merges by the last CTA of each group and the last group ->
+ * this shard's partial
+ *   part_out (dev) = [m_r, Z_r, nonfinite_r, best_index_r, N_r[H*n]]
+ * (the record ranks all-gather).  m_offset = global
+ * index of local sample 0.  costs (dev, M f64) / flags (dev, M u8) optional. */
 size_t vpb_smpc_workspace_bytes(int64_t M, int64_t H, int64_t n);
 int64_t vpb_smpc_partial_len(int64_t H, int64_t n);
 int vpb_smpc_partial(const vpb_problem *prob, const vpb_field *field,
@@ -217,14 +221,21 @@ int vpb_smpc_partial(const vpb_problem *prob, const vpb_field *field,
                      double *costs, uint8_t *flags, double *part_out,
                      void *workspace, size_t workspace_bytes, void *stream);
 
-/* Merge R shard partials (R x partial_len, dev, fixed rank order) and finish
- * the step: U* = nominal + N/Z, then re-evaluate U* (M = 1) for the
- * diagnostics, clip the command and shift the warm start
- * (vp/planner.py:614-629).  out (dev) layout:
+/* Single-device SMPC step, fully fused in one launch: the partial above,
+ * then (by the last CTA) U* = nominal + N/Z, the clipped command, the
+ * shifted warm start and the M = 1 re-evaluation of U* (vp/planner.py:
+ * 614-629).  out (dev) layout (vpb_smpc_out_len doubles):
  *   [U* (H*n), command (n), next_nominal (H*n), weighted_cost, terms[6],
  *    best_cost, Z, nonfinite_count, best_index]
  * (weighted_cost = +inf when the re-evaluation hits the log singularity). */
 int64_t vpb_smpc_out_len(int64_t H, int64_t n);
+int vpb_smpc_step(const vpb_problem *prob, const vpb_field *field,
+                  const void *eps, int dtype, const double *nominal, int64_t M,
+                  int precision, double *costs, uint8_t *flags, double *out,
+                  void *workspace, size_t workspace_bytes, void *stream);
+
+/* Multi-device finish: merge R rank partials (R x partial_len, dev) in rank
+ * order and run the same tail as vpb_smpc_step into `out`. */
 size_t vpb_smpc_finish_workspace_bytes(int64_t n_parts, int64_t H, int64_t n);
 int vpb_smpc_finish(const vpb_problem *prob, const vpb_field *field,
                     const double *partials, int64_t n_parts,
@@ -237,12 +248,13 @@ int vpb_smpc_finish(const vpb_problem *prob, const vpb_field *field,
 /* Counter-based Philox4x32-10 stream keyed by (seed, sample index), standard
  * normals, moving-average smoothing over `window` (rows scaled 1/sqrt(count)),
  * times sigma[j]; sample 0 is the zero perturbation.  Statistically (not
- * bitwise) equivalent to numpy's Philox stream.  m_offset = global index of
- * local sample 0 (for sharded sampling).  out (dev) M x H x n of dtype. */
-int vpb_sample_perturbations(uint64_t seed, int64_t m_offset, int64_t M,
-                             int64_t H, int64_t n, int64_t window,
-                             const double *sigma, int dtype, void *out,
-                             void *stream);
+ * bitwise) equivalent to numpy's Philox stream.  seed_dev (dev, optional)
+ * overrides `seed` (graph replays).  m_offset = global index of local sample
+ * 0 (sharded sampling).  out (dev) M x H x n of dtype. */
+int vpb_sample_perturbations(uint64_t seed, const uint64_t *seed_dev,
+                             int64_t m_offset, int64_t M, int64_t H, int64_t n,
+                             int64_t window, const double *sigma, int dtype,
+                             void *out, void *stream);
 
 #ifdef __cplusplus
 }

@@ -74,7 +74,7 @@ class VpbProblem(ctypes.Structure):
         ("acc_limit", _d * MAX_JOINTS), ("q_ref", _d * MAX_JOINTS),
         ("q0", _d * MAX_JOINTS), ("qd0", _d * MAX_JOINTS),
         ("w_env", _d), ("w_self", _d), ("w_q", _d), ("w_qd", _d), ("w_qdd", _d),
-        ("w_s", _d), ("w_ns", _d), ("d_act", _d), ("lam", _d),
+        ("w_s", _d), ("w_ns", _d), ("d_act", _d), ("lam", _d), ("dyn_state", _p),
     ]
 
 
@@ -104,10 +104,12 @@ SIGNATURES = {
     "vpb_smpc_partial": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _p, ctypes.c_int, _p, _i64, _i64,
                                         ctypes.c_int, _p, _p, _p, _p, _sz, _p]),
     "vpb_smpc_out_len": (_i64, [_i64, _i64]),
+    "vpb_smpc_step": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _p, ctypes.c_int, _p, _i64, ctypes.c_int, _p,
+                                     _p, _p, _p, _sz, _p]),
     "vpb_smpc_finish_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "vpb_smpc_finish": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _p, _i64, _p, ctypes.c_int, _p, _p,
                                        _sz, _p]),
-    "vpb_sample_perturbations": (ctypes.c_int, [ctypes.c_uint64, _i64, _i64, _i64, _i64, _i64, _p,
+    "vpb_sample_perturbations": (ctypes.c_int, [ctypes.c_uint64, _p, _i64, _i64, _i64, _i64, _i64, _p,
                                                 ctypes.c_int, _p, _p]),
 }
 

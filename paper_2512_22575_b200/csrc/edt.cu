@@ -256,9 +256,11 @@ __global__ void __launch_bounds__(256) edt_pass_z_scan(const uint32_t *__restric
                                                        int64_t words_z, int64_t lo0, int64_t lo1, int lo2,
                                                        int64_t n0, int64_t n1, int n2, uint16_t *__restrict__ out) {
   const int lane = threadIdx.x & 31;
-  const int64_t line = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (line >= n0 * n1) return;
-  const int64_t i0 = line / n1, i1 = line - i0 * n1;
+  // grid: (ceil(n1 / 8), n0)
+  const int64_t i1 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i1 >= n1) return;
+  const int64_t i0 = blockIdx.y;
+  const int64_t line = i0 * n1 + i1;
   const uint32_t *w = bits + ((lo0 + i0) * gy + (lo1 + i1)) * words_z;
   const int nw = (n2 + 31) >> 5;
   uint32_t word = 0;
@@ -343,10 +345,9 @@ __global__ void __launch_bounds__(32) edt_pass_fh_smem(const TIn *__restrict__ i
                                                        int64_t stride) {
   extern __shared__ uint32_t tile[];  // [len][32]
   const int lane = threadIdx.x;
-  const int zchunks = (n2 + 31) >> 5;
-  const int64_t a = blockIdx.x / zchunks;
-  const int z = (int)(blockIdx.x - a * zchunks) * 32 + lane;
-  if (a >= n_outer) return;
+  // grid: (zchunks, n_outer)
+  const int64_t a = blockIdx.y;
+  const int z = (int)blockIdx.x * 32 + lane;
   const bool act = z < n2;
   const int64_t base = a * outer_stride + (act ? z : 0);
   const TIn *src = in + base;
@@ -430,12 +431,13 @@ __global__ void __launch_bounds__(32) edt_pass_fh_smem(const TIn *__restrict__ i
 template <typename TIn, typename TOut>
 static int launch_fh_smem(const TIn *in, TOut *out, int64_t n_outer, int64_t outer_stride, int64_t n2, int64_t len,
                           int64_t stride, cudaStream_t s) {
-  const int64_t blocks = n_outer * ((n2 + 31) >> 5);
-  if (blocks == 0) return VPB_OK;
+  if (n_outer == 0) return VPB_OK;
+  VPB_REQUIRE(n_outer <= 65535, "EDT box side too long for the grid y dimension");
   const size_t smem = (size_t)len * 32 * sizeof(uint32_t);
   auto kern = edt_pass_fh_smem<TIn, TOut>;
   if (smem > 48 * 1024) VPB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  kern<<<(unsigned)blocks, 32, smem, s>>>(in, out, n_outer, outer_stride, (int)n2, (int)len, stride);
+  kern<<<dim3((unsigned)((n2 + 31) >> 5), (unsigned)n_outer), 32, smem, s>>>(in, out, n_outer, outer_stride, (int)n2,
+                                                                              (int)len, stride);
   return check_launch("edt_pass_fh_smem");
 }
 
@@ -488,7 +490,7 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], dou
   if (use_bits) {
     VPB_REQUIRE(grid->occ_bits, "use_bits set but grid->occ_bits is null");
     if (n[2] <= 1024) {
-      edt_pass_z_scan<<<(unsigned)ceil_div(lines_z, 8), 256, 0, s>>>(grid->occ_bits, grid->dims[1],
+      edt_pass_z_scan<<<dim3((unsigned)ceil_div(n[1], 8), (unsigned)n[0]), 256, 0, s>>>(grid->occ_bits, grid->dims[1],
                                                                      ceil_div(grid->dims[2], 32), lo[0], lo[1],
                                                                      (int)lo[2], n[0], n[1], (int)n[2], dz);
     } else {

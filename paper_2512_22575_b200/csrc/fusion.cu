@@ -47,14 +47,13 @@ __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a,
 // grid: x = lo0 + blockIdx.y ... flattened: blockIdx.x over (i0, i1, zword)
 __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ FusionArgs A) {
   const int lane = threadIdx.x & 31;
-  const int64_t warp_global = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int64_t per_x = A.n1 * A.wz_count;
-  const int64_t total = A.n0 * per_x;
-  if (warp_global >= total) return;
-  const int64_t i0 = warp_global / per_x;
-  const int64_t rem = warp_global - i0 * per_x;
-  const int64_t i1 = rem / A.wz_count;
-  const int64_t wz = A.wz_begin + (rem - i1 * A.wz_count);
+  // grid: (ceil(n1 * wz_count / 8), n0); 32-bit index math only
+  const int per_x = (int)(A.n1 * A.wz_count);
+  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= per_x) return;
+  const int64_t i0 = blockIdx.y;
+  const int i1 = w / (int)A.wz_count;
+  const int64_t wz = A.wz_begin + (w - i1 * (int)A.wz_count);
   const int64_t x = A.lo0 + i0, y = A.lo1 + i1;
   const int64_t z = wz * 32 + lane;
   const bool in_box = (z >= A.lo2) && (z < A.lo2 + A.n2);
@@ -362,8 +361,9 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3
   A.hf = (float)A.height;
   // the fp32 prefilter assumes an orthonormal world->camera rotation and a
   // scene within float range; anything else simply takes the exact path
-  const int64_t warps = A.n0 * A.n1 * A.wz_count;
-  fuse_kernel<<<(unsigned)ceil_div(warps, 8), 256, 0, as_stream(stream)>>>(A);
+  VPB_REQUIRE(A.n0 <= 65535 && A.n1 * A.wz_count < (1ll << 30), "box too large for the fusion grid");
+  dim3 launch_grid((unsigned)ceil_div(A.n1 * A.wz_count, 8), (unsigned)A.n0);
+  fuse_kernel<<<launch_grid, 256, 0, as_stream(stream)>>>(A);
   return check_launch("fuse_kernel");
 }
 

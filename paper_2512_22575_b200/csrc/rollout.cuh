@@ -46,6 +46,16 @@ struct Prob {
   T pi_limit;  // pi - _PI_MARGIN in T
 };
 
+// Per-call state (start state and goal).  Read from a device buffer when the
+// caller provides one (graph replays update it with one tiny H2D copy), else
+// from the launch parameters.  Device layout: [q0 (n), qd0 (n), goal_r (9),
+// goal_t (3)] as f64.
+template <typename T>
+struct Dyn {
+  T q0[kMaxJ], qd0[kMaxJ];
+  T goal_r[9], goal_t[3];
+};
+
 template <typename T>
 __device__ __forceinline__ T tsqrt(T x);
 template <>
@@ -212,8 +222,9 @@ __device__ __forceinline__ void fk_link(const Prob<T> &P, int i, T q, T R[9], T 
 // log-map singularity.  fp32 uses theta = atan2(|vee|, cos) (stable at small
 // angles); fp64 follows the reference's acos exactly.
 template <typename T>
-__device__ __forceinline__ bool pose_quad(const Prob<T> &P, const T R[9], const T t[3], const T *W, T *out) {
-  const T *G = P.goal_r;
+__device__ __forceinline__ bool pose_quad(const Prob<T> &P, const Dyn<T> &D, const T R[9], const T t[3], const T *W,
+                                          T *out) {
+  const T *G = D.goal_r;
   const T d00 = G[0] * R[0] + G[3] * R[3] + G[6] * R[6];
   const T d01 = G[0] * R[1] + G[3] * R[4] + G[6] * R[7];
   const T d02 = G[0] * R[2] + G[3] * R[5] + G[6] * R[8];
@@ -223,7 +234,7 @@ __device__ __forceinline__ bool pose_quad(const Prob<T> &P, const T R[9], const 
   const T d20 = G[2] * R[0] + G[5] * R[3] + G[8] * R[6];
   const T d21 = G[2] * R[1] + G[5] * R[4] + G[8] * R[7];
   const T d22 = G[2] * R[2] + G[5] * R[5] + G[8] * R[8];
-  const T rx = t[0] - P.goal_t[0], ry = t[1] - P.goal_t[1], rz = t[2] - P.goal_t[2];
+  const T rx = t[0] - D.goal_t[0], ry = t[1] - D.goal_t[1], rz = t[2] - D.goal_t[2];
   const T tx = G[0] * rx + G[3] * ry + G[6] * rz;
   const T ty = G[1] * rx + G[4] * ry + G[7] * rz;
   const T tz = G[2] * rx + G[5] * ry + G[8] * rz;

@@ -13,6 +13,7 @@ namespace vpb {
 
 struct SamplerArgs {
   uint64_t seed;
+  const uint64_t *seed_dev;  // optional: seed read from device memory (graph replays)
   int64_t m_offset, M, H, n, window;
   double sigma[VPB_MAX_JOINTS];
   void *out;
@@ -42,6 +43,16 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint32_t k0, uint32_t 
   return make_uint4(c0, c1, c2, c3);
 }
 
+__device__ __forceinline__ void box_muller_f(uint32_t a, uint32_t b, float &z0, float &z1) {
+  const float u1 = ((float)(a >> 8) + 0.5f) * 5.9604644775390625e-08f;  // (0,1), 24-bit
+  const float u2 = ((float)(b >> 8) + 0.5f) * 5.9604644775390625e-08f;
+  const float r = sqrtf(-2.0f * logf(u1));
+  float s, c;
+  sincospif(2.0f * u2, &s, &c);
+  z0 = r * c;
+  z1 = r * s;
+}
+
 __device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, double &z0, double &z1) {
   const double u1 = ((double)a + 0.5) * 2.3283064365386963e-10;  // (0,1)
   const double u2 = ((double)b + 0.5) * 2.3283064365386963e-10;
@@ -61,14 +72,23 @@ __global__ void __launch_bounds__(256) sampler_kernel(const __grid_constant__ Sa
   double *r = raw + (size_t)warp * hn;
   if (mloc >= A.M) return;
   const int64_t mg = A.m_offset + mloc;
-  const uint32_t k0 = (uint32_t)A.seed ^ (uint32_t)(mg * 0x9E3779B97F4A7C15ull);
-  const uint32_t k1 = (uint32_t)(A.seed >> 32) ^ (uint32_t)((uint64_t)mg >> 32) ^ 0x85EBCA6Bu;
+  const uint64_t seed = A.seed_dev ? *A.seed_dev : A.seed;
+  const uint32_t k0 = (uint32_t)seed ^ (uint32_t)((uint64_t)mg * 0x9E3779B97F4A7C15ull);
+  const uint32_t k1 = (uint32_t)(seed >> 32) ^ (uint32_t)((uint64_t)mg >> 32) ^ 0x85EBCA6Bu;
   const int64_t ncalls = (hn + 3) / 4;
   for (int64_t c = lane; c < ncalls; c += 32) {
     const uint4 x = philox4x32_10(make_uint4((uint32_t)c, (uint32_t)mg, (uint32_t)(mg >> 32), 0x5eedu), k0, k1);
     double z[4];
-    box_muller(x.x, x.y, z[0], z[1]);
-    box_muller(x.z, x.w, z[2], z[3]);
+    if (A.dtype == VPB_DTYPE_F32) {
+      float f[4];
+      box_muller_f(x.x, x.y, f[0], f[1]);
+      box_muller_f(x.z, x.w, f[2], f[3]);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) z[t] = f[t];
+    } else {
+      box_muller(x.x, x.y, z[0], z[1]);
+      box_muller(x.z, x.w, z[2], z[3]);
+    }
 #pragma unroll
     for (int t = 0; t < 4; ++t)
       if (4 * c + t < hn) r[4 * c + t] = z[t];
@@ -103,8 +123,9 @@ __global__ void __launch_bounds__(256) sampler_kernel(const __grid_constant__ Sa
 
 using namespace vpb;
 
-extern "C" int vpb_sample_perturbations(uint64_t seed, int64_t m_offset, int64_t M, int64_t H, int64_t n,
-                                        int64_t window, const double *sigma, int dtype, void *out, void *stream) {
+extern "C" int vpb_sample_perturbations(uint64_t seed, const uint64_t *seed_dev, int64_t m_offset, int64_t M,
+                                        int64_t H, int64_t n, int64_t window, const double *sigma, int dtype,
+                                        void *out, void *stream) {
   VPB_REQUIRE(out && sigma && M >= 0 && H >= 1 && n >= 1 && n <= VPB_MAX_JOINTS && m_offset >= 0,
               "bad arguments to vpb_sample_perturbations");
   VPB_REQUIRE(dtype == VPB_DTYPE_F32 || dtype == VPB_DTYPE_F64, "bad dtype");
@@ -112,6 +133,7 @@ extern "C" int vpb_sample_perturbations(uint64_t seed, int64_t m_offset, int64_t
   SamplerArgs A;
   memset(&A, 0, sizeof(A));
   A.seed = seed;
+  A.seed_dev = seed_dev;
   A.m_offset = m_offset;
   A.M = M;
   A.H = H;

@@ -55,6 +55,8 @@ class ShardedSMPC:
             eps = pl.sample_device(rng_seed, m_offset=self.rank * self.m_local, samples=self.m_local)
         else:
             eps = perturbations
+        if self.world == 1:
+            return pl.smpc_step_device(state, goal, snap, nominal_dev, eps)  # one fused launch
         part, _, _ = pl.smpc_partial_device(state, goal, snap, nominal_dev, eps, m_offset=self.rank * self.m_local)
         parts = exchange_partials(part, self.world, self.group)
         return pl.smpc_finish_device(state, goal, snap, nominal_dev, parts)

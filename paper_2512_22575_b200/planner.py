@@ -226,11 +226,16 @@ class Planner:
         self._acc_limits = chain.acceleration_limits()
         self._base = pack_problem(chain, model, params)
 
-    def problem(self, state: JointState, goal: RigidTransform, horizon: int | None = None) -> VpbProblem:
+    def problem(self, state: JointState | None, goal: RigidTransform | None, horizon: int | None = None,
+                dyn: torch.Tensor | None = None) -> VpbProblem:
         P = VpbProblem()
         ctypes.memmove(ctypes.byref(P), ctypes.byref(self._base), ctypes.sizeof(VpbProblem))
         if horizon is not None:
             P.horizon = int(horizon)
+        if dyn is not None:
+            P.dyn_state = D.ptr(dyn)
+        if state is None:
+            return P
         q0 = np.asarray(state.q, dtype=float).reshape(-1)
         qd0 = np.asarray(state.qd, dtype=float).reshape(-1)
         if q0.shape != (self.chain.dof,) or qd0.shape != (self.chain.dof,):
@@ -300,42 +305,65 @@ class Planner:
         )
 
     # -- smpc step -------------------------------------------------------------
-    def sample_device(self, rng_seed: int, m_offset: int = 0, samples: int | None = None) -> torch.Tensor:
+    def sample_device(self, rng_seed: int, m_offset: int = 0, samples: int | None = None,
+                      seed_dev: torch.Tensor | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+        """On-device perturbations (M, H, n) in the planner's noise dtype."""
         p = self.params
         m = p.samples if samples is None else int(samples)
-        out = torch.empty((m, p.horizon, self.chain.dof), dtype=self._eps_dtype, device=self.device)
+        if out is None:
+            out = torch.empty((m, p.horizon, self.chain.dof), dtype=self._eps_dtype, device=self.device)
         sig = np.ascontiguousarray(p.sigma, dtype=np.float64)
         check(load().vpb_sample_perturbations(
-            int(rng_seed) & 0xFFFFFFFFFFFFFFFF, int(m_offset), m, p.horizon, self.chain.dof, p.noise_window,
-            D.host_ptr(sig), DTYPE_F32 if self._eps_dtype == torch.float32 else DTYPE_F64, D.ptr(out),
+            int(rng_seed) & 0xFFFFFFFFFFFFFFFF, D.ptr(seed_dev), int(m_offset), m, p.horizon, self.chain.dof,
+            p.noise_window, D.host_ptr(sig), DTYPE_F32 if out.dtype == torch.float32 else DTYPE_F64, D.ptr(out),
             D.stream(self.device)), "sample_perturbations")
         return out
 
-    def smpc_partial_device(self, state, goal, snap, nominal_dev: torch.Tensor, eps_dev: torch.Tensor,
-                            m_offset: int = 0):
-        """Rollout + this shard's softmin partial (device, no sync).
-        Returns (partial (L,) f64, costs (M,), flags (M,))."""
-        m, h, n = eps_dev.shape
-        P = self.problem(state, goal, horizon=h)
+    def _smpc_ws(self, m: int, h: int) -> torch.Tensor:
         L = load()
-        plen = int(L.vpb_smpc_partial_len(h, n))
-        part = torch.empty(plen, dtype=torch.float64, device=self.device)
+        return D.Workspace.get(self.device, f"smpc-{m}-{h}", int(L.vpb_smpc_workspace_bytes(m, h, self.chain.dof)))
+
+    def smpc_partial_device(self, state, goal, snap, nominal_dev: torch.Tensor, eps_dev: torch.Tensor,
+                            m_offset: int = 0, dyn: torch.Tensor | None = None):
+        """Rollout + this shard's merged softmin partial in one launch (device,
+        no sync).  Returns (partial (L,) f64, costs (M,), flags (M,))."""
+        m, h, n = eps_dev.shape
+        P = self.problem(state, goal, horizon=h, dyn=dyn)
+        L = load()
+        part = torch.empty(int(L.vpb_smpc_partial_len(h, n)), dtype=torch.float64, device=self.device)
         costs = torch.empty(m, dtype=torch.float64, device=self.device)
         flags = torch.empty(m, dtype=torch.uint8, device=self.device)
-        ws_bytes = int(L.vpb_smpc_workspace_bytes(m, h, n))
-        ws = D.Workspace.get(self.device, "smpc", ws_bytes)
+        ws = self._smpc_ws(m, h)
         dtype = DTYPE_F32 if eps_dev.dtype == torch.float32 else DTYPE_F64
         check(L.vpb_smpc_partial(P, _field_struct(snap), D.ptr(eps_dev), dtype, D.ptr(nominal_dev), m, int(m_offset),
-                                 self._prec,
-                                 D.ptr(costs), D.ptr(flags), D.ptr(part), D.ptr(ws), ws.numel(),
+                                 self._prec, D.ptr(costs), D.ptr(flags), D.ptr(part), D.ptr(ws), ws.numel(),
                                  D.stream(self.device)), "smpc_partial")
         return part, costs, flags
 
-    def smpc_finish_device(self, state, goal, snap, nominal_dev: torch.Tensor, partials: torch.Tensor):
-        """Merge shard partials (R, L) in fixed order and finish the step on
-        the device.  Returns the packed output vector (see vpb_smpc_out_len)."""
+    def smpc_step_device(self, state, goal, snap, nominal_dev: torch.Tensor, eps_dev: torch.Tensor,
+                         out: torch.Tensor | None = None, costs: torch.Tensor | None = None,
+                         dyn: torch.Tensor | None = None) -> torch.Tensor:
+        """Whole single-device step in ONE kernel launch (rollout, softmin
+        partials, fixed-order merges, U*, clip, shift, re-evaluation).
+        Returns the packed output vector (vpb_smpc_out_len doubles)."""
+        m, h, n = eps_dev.shape
+        P = self.problem(state, goal, horizon=h, dyn=dyn)
+        L = load()
+        if out is None:
+            out = torch.empty(int(L.vpb_smpc_out_len(h, n)), dtype=torch.float64, device=self.device)
+        ws = self._smpc_ws(m, h)
+        dtype = DTYPE_F32 if eps_dev.dtype == torch.float32 else DTYPE_F64
+        check(L.vpb_smpc_step(P, _field_struct(snap), D.ptr(eps_dev), dtype, D.ptr(nominal_dev), m, self._prec,
+                              D.ptr(costs), None, D.ptr(out), D.ptr(ws), ws.numel(), D.stream(self.device)),
+              "smpc_step")
+        return out
+
+    def smpc_finish_device(self, state, goal, snap, nominal_dev: torch.Tensor, partials: torch.Tensor,
+                           dyn: torch.Tensor | None = None):
+        """Merge rank partials (R, L) in rank order and finish the step on the
+        device.  Returns the packed output vector (vpb_smpc_out_len)."""
         h, n = nominal_dev.shape
-        P = self.problem(state, goal, horizon=h)
+        P = self.problem(state, goal, horizon=h, dyn=dyn)
         L = load()
         out = torch.empty(int(L.vpb_smpc_out_len(h, n)), dtype=torch.float64, device=self.device)
         parts = partials.reshape(-1, int(L.vpb_smpc_partial_len(h, n))).contiguous()
@@ -385,8 +413,7 @@ class Planner:
             eps_dev = _as_device(perturbations, self.device, self._eps_dtype)
             if tuple(eps_dev.shape) != (eps_dev.shape[0], h, n):
                 raise DimensionMismatch("perturbations must be (M, H, n)")
-        part, _, _ = self.smpc_partial_device(state, goal, snap, nom_dev, eps_dev)
-        out = self.smpc_finish_device(state, goal, snap, nom_dev, part.reshape(1, -1))
+        out = self.smpc_step_device(state, goal, snap, nom_dev, eps_dev)
         return self.unpack_step(out.cpu().numpy(), state, goal, h)
 
     def integrate(self, state: JointState, command: np.ndarray) -> JointState:
@@ -451,7 +478,83 @@ def sample_perturbations(params: PlannerParams, rng_seed: int, device=None, dtyp
     out = torch.empty((params.samples, params.horizon, params.dof), dtype=dtype, device=dev)
     sig = np.ascontiguousarray(params.sigma, dtype=np.float64)
     check(load().vpb_sample_perturbations(
-        int(rng_seed) & 0xFFFFFFFFFFFFFFFF, 0, params.samples, params.horizon, params.dof, params.noise_window,
+        int(rng_seed) & 0xFFFFFFFFFFFFFFFF, None, 0, params.samples, params.horizon, params.dof, params.noise_window,
         D.host_ptr(sig), DTYPE_F32 if dtype == torch.float32 else DTYPE_F64, D.ptr(out), D.stream(dev)),
         "sample_perturbations")
     return out
+
+
+class SmpcGraph:
+    """One single-device SMPC step captured as a CUDA graph.
+
+    The graph holds: host->device copy of the per-call block (start state,
+    goal, seed, nominal) from pinned memory, the on-device sampler, the fused
+    one-kernel SMPC step and the device->host copy of the packed result.  A
+    call writes the pinned block, replays the graph and waits for the result,
+    so the host does no per-launch work.  The distance field is part of the
+    captured launch; use one graph per field buffer (the mapper's pipeline
+    keeps its field buffer fixed).
+    """
+
+    def __init__(self, planner: Planner, snap, samples: int | None = None):
+        self.pl = planner
+        p = planner.params
+        self.m = int(samples or p.samples)
+        self.h, self.n = p.horizon, planner.chain.dof
+        dev = planner.device
+        n = self.n
+        L = load()
+        self.dyn_len = 2 * n + 12
+        # [dyn (2n + 12) | seed (1, as uint64 bits) | nominal (H n)]
+        self.block_len = self.dyn_len + 1 + self.h * n
+        self.host_in = torch.zeros(self.block_len, dtype=torch.float64).pin_memory()
+        self.dev_in = torch.zeros(self.block_len, dtype=torch.float64, device=dev)
+        self.out_len = int(L.vpb_smpc_out_len(self.h, n))
+        self.dev_out = torch.zeros(self.out_len, dtype=torch.float64, device=dev)
+        self.host_out = torch.zeros(self.out_len, dtype=torch.float64).pin_memory()
+        self.eps = torch.empty((self.m, self.h, n), dtype=planner._eps_dtype, device=dev)
+        self.snap = snap
+        self._seed_view = self.dev_in[self.dyn_len:self.dyn_len + 1].view(torch.int64)
+        self._nom_view = self.dev_in[self.dyn_len + 1:].view(self.h, n)
+        self._dyn_view = self.dev_in[:self.dyn_len]
+        self.planner_ws = planner._smpc_ws(self.m, self.h)
+        # warm once outside capture (workspace, kernel attributes)
+        self._enqueue(copy_out=False)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(self.graph, stream=s):
+                self._enqueue(copy_out=True)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+
+    def _enqueue(self, copy_out: bool):
+        self.dev_in.copy_(self.host_in, non_blocking=True)
+        self.pl.sample_device(0, samples=self.m, seed_dev=self._seed_view, out=self.eps)
+        self.pl.smpc_step_device(None, None, self.snap, self._nom_view, self.eps, out=self.dev_out,
+                                 dyn=self._dyn_view)
+        if copy_out:
+            self.host_out.copy_(self.dev_out, non_blocking=True)
+
+    def stage(self, state: JointState, goal: RigidTransform, nominal, rng_seed: int) -> None:
+        n = self.n
+        h = self.host_in.numpy()
+        h[:n] = np.asarray(state.q, dtype=float)
+        h[n:2 * n] = np.asarray(state.qd, dtype=float)
+        h[2 * n:2 * n + 9] = np.asarray(goal.rotation.matrix, dtype=float).reshape(-1)
+        h[2 * n + 9:2 * n + 12] = np.asarray(goal.translation, dtype=float)
+        h[self.dyn_len:self.dyn_len + 1].view(np.uint64)[0] = np.uint64(int(rng_seed) & 0xFFFFFFFFFFFFFFFF)
+        nom = np.zeros((self.h, n)) if nominal is None else np.asarray(nominal, dtype=float)
+        h[self.dyn_len + 1:] = nom.reshape(-1)
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    def step(self, state: JointState, goal: RigidTransform, nominal, rng_seed: int) -> StepResult:
+        """Public-API step with host buffers (same contract as Planner.smpc_step)."""
+        self.stage(state, goal, nominal, rng_seed)
+        self.graph.replay()
+        torch.cuda.current_stream(self.pl.device).synchronize()
+        return self.pl.unpack_step(self.host_out.numpy().copy(), state, goal, self.h)

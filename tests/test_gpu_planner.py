@@ -316,3 +316,40 @@ def test_fixed_point_at_goal(pk):
         res = planner.Planner(chain, model, params, prec).smpc_step(robot.JointState.resting(q), goal, None, None, 0)
         np.testing.assert_allclose(res.command, 0.0, atol=1e-9)
         np.testing.assert_allclose(res.next_nominal, 0.0, atol=1e-9)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_fused_step_equals_partial_finish_and_graph(pk, precision):
+    """The one-launch SMPC step, the partial + finish path and the CUDA-graph
+    replay (per-call state from device memory) give the same step."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.geometry import RigidTransform
+
+    chain, model = config.robot_7dof()
+    grid = mapping.VoxelGrid((-1.0, -1.0, 0.0), 0.05, (30, 30, 30))
+    occ = np.zeros((30, 30, 30), bool)
+    occ[12:16, 12:16, 10:14] = True
+    grid.set_log_odds(np.where(occ, 3.5, 0.0))
+    field = mapping.edt_3d(grid, outside_default=0.8)
+    for m, h in ((1000, 20), (4096, 32), (300, 64)):
+        params = config.planner_params(7, {"samples": m, "horizon": h})
+        pl = planner.Planner(chain, model, params, precision)
+        state = robot.JointState(np.full(7, 0.1), np.linspace(-0.2, 0.2, 7), np.zeros(7))
+        goal = RigidTransform.from_vec7([0.3, -0.2, 0.7, 0.9, 0.1, 0.3, -0.2])
+        nom = torch.from_numpy(0.2 * np.cos(np.arange(h * 7)).reshape(h, 7)).cuda()
+        eps = pl.sample_device(99)
+        fused = pl.smpc_step_device(state, goal, field, nom, eps).cpu().numpy()
+        part, _, _ = pl.smpc_partial_device(state, goal, field, nom, eps)
+        split = pl.smpc_finish_device(state, goal, field, nom, part.reshape(1, -1)).cpu().numpy()
+        np.testing.assert_allclose(fused, split, rtol=1e-12, atol=1e-14)
+        g = planner.SmpcGraph(pl, field)
+        res = g.step(state, goal, nom.cpu().numpy(), 99)
+        direct = pl.smpc_step(state, goal, field, nom.cpu().numpy(), 99)
+        np.testing.assert_array_equal(res.command, direct.command)
+        np.testing.assert_array_equal(res.next_nominal, direct.next_nominal)
+        assert res.diagnostics.weighted_cost == direct.diagnostics.weighted_cost
+        # a second replay with a new state/seed follows the staged inputs
+        state2 = robot.JointState.resting(np.full(7, -0.2))
+        res2 = g.step(state2, goal, None, 7)
+        direct2 = pl.smpc_step(state2, goal, field, None, 7)
+        np.testing.assert_array_equal(res2.command, direct2.command)
