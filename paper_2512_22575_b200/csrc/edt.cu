@@ -441,6 +441,344 @@ static int launch_fh_smem(const TIn *in, TOut *out, int64_t n_outer, int64_t out
   return check_launch("edt_pass_fh_smem");
 }
 
+// ---------------------------------------------------------------------------
+// Segmented FH line kernels (the production path for lines <= 1024).
+//
+// A 128-thread CTA owns 32 lines (lanes over the contiguous z axis) staged as
+// a [len][32] u32 tile in shared memory.  Each line is split into KSEG = 4
+// segments handled by 4 threads: each builds the lower envelope of its
+// segment in place (stack entry (f << 10) | v over consumed input slots),
+// the envelopes are merged pairwise (the merged envelope of two runs is a
+// prefix of the left run plus a suffix of the right one, found by dropping
+// boundary parabolas that are dominated by their neighbours), and every
+// thread then locates the parabola covering its first output by binary
+// search and sweeps its segment.  Tile columns are rotated by 8 per segment
+// so the 4 threads of a line hit different banks.
+// ---------------------------------------------------------------------------
+constexpr int KSEG = 4;
+constexpr int LINES = 32;
+constexpr int ETHREADS = LINES * KSEG;
+
+struct SegLine {
+  int lo[KSEG], hi[KSEG];
+};
+
+__device__ __forceinline__ int tslot(int line, int seg, int row) { return row * 32 + ((line + 8 * seg) & 31); }
+
+struct Elem {
+  int v, f, F;
+};
+
+__device__ __forceinline__ Elem elem_at(const uint32_t *tile, int line, int B, int seg, int idx) {
+  const uint32_t e = tile[tslot(line, seg, seg * B + idx)];
+  Elem r;
+  r.v = (int)(e & 1023u);
+  r.f = (int)(e >> 10);
+  r.F = r.f + r.v * r.v;
+  return r;
+}
+
+// s(a, b) < q  <=>  F_b - F_a < 2 q (v_b - v_a)
+__device__ __forceinline__ bool boundary_lt(const Elem &a, const Elem &b, int q) {
+  return (long long)(b.F - a.F) < 2ll * q * (b.v - a.v);
+}
+
+// dominated(l, p, r): s(l, p) >= s(p, r)
+__device__ __forceinline__ bool dominated(const Elem &l, const Elem &p, const Elem &r) {
+  return (long long)(p.F - l.F) * (r.v - p.v) >= (long long)(r.F - p.F) * (p.v - l.v);
+}
+
+// previous / next non-empty element in segment order
+__device__ __forceinline__ bool prev_elem(const SegLine &S, int seg, int idx, int first_seg, int &ps, int &pi) {
+  if (idx > S.lo[seg]) {
+    ps = seg;
+    pi = idx - 1;
+    return true;
+  }
+  for (int t = seg - 1; t >= first_seg; --t)
+    if (S.hi[t] > S.lo[t]) {
+      ps = t;
+      pi = S.hi[t] - 1;
+      return true;
+    }
+  return false;
+}
+
+__device__ __forceinline__ bool next_elem(const SegLine &S, int seg, int idx, int last_seg, int &ns, int &ni) {
+  if (idx + 1 < S.hi[seg]) {
+    ns = seg;
+    ni = idx + 1;
+    return true;
+  }
+  for (int t = seg + 1; t <= last_seg; ++t)
+    if (S.hi[t] > S.lo[t]) {
+      ns = t;
+      ni = S.lo[t];
+      return true;
+    }
+  return false;
+}
+
+// Merge left run (segments a..b) with right run (b+1..c) of one line.
+__device__ void merge_runs(const uint32_t *tile, int line, int B, SegLine &S, int a, int b, int c) {
+  // last element of the left run, first of the right run
+  int ls = -1, li = 0, rs = -1, ri = 0;
+  for (int t = b; t >= a; --t)
+    if (S.hi[t] > S.lo[t]) {
+      ls = t;
+      li = S.hi[t] - 1;
+      break;
+    }
+  for (int t = b + 1; t <= c; ++t)
+    if (S.hi[t] > S.lo[t]) {
+      rs = t;
+      ri = S.lo[t];
+      break;
+    }
+  if (ls < 0 || rs < 0) return;
+  while (true) {
+    bool changed = false;
+    const Elem L1 = elem_at(tile, line, B, ls, li);
+    const Elem R1 = elem_at(tile, line, B, rs, ri);
+    int ps, pi;
+    if (prev_elem(S, ls, li, a, ps, pi)) {
+      const Elem L2 = elem_at(tile, line, B, ps, pi);
+      if (dominated(L2, L1, R1)) {
+        S.hi[ls] = li;  // drop the left run's last element
+        ls = ps;
+        li = pi;
+        changed = true;
+      }
+    }
+    if (!changed) {
+      int ns, ni;
+      if (next_elem(S, rs, ri, c, ns, ni)) {
+        const Elem R2 = elem_at(tile, line, B, ns, ni);
+        if (dominated(L1, R1, R2)) {
+          S.lo[rs] = ri + 1;  // drop the right run's first element
+          rs = ns;
+          ri = ni;
+          changed = true;
+        }
+      }
+    }
+    if (!changed) break;
+  }
+}
+
+template <typename TOut>
+__device__ __forceinline__ void store_dist(TOut *p, int v);
+template <>
+__device__ __forceinline__ void store_dist<int32_t>(int32_t *p, int v) {
+  *p = v < 0 ? kNoSrc32 : v;
+}
+template <>
+__device__ __forceinline__ void store_dist<float>(float *p, int v) {
+  *p = v < 0 ? __int_as_float(0x7f800000) : (float)v;
+}
+
+// Envelope + output for the tile (called by all ETHREADS threads after the
+// tile is filled and synchronised).  dst(line) + q * stride receives output q.
+template <typename TOut>
+__device__ void segmented_fh(uint32_t *tile, SegLine *segs, int len, int nlines_active, TOut *dst_base,
+                             int64_t stride) {
+  const int tid = threadIdx.x;
+  const int s = tid >> 5;          // segment = warp index
+  const int line = tid & 31;       // z lane
+  const int B = (len + KSEG - 1) / KSEG;
+  const int q0 = s * B, q1 = min(len, q0 + B);
+  const bool act = line < nlines_active;
+  // ---- forward sweep on this segment (stack in place) ----
+  int k = -1;
+  if (act) {
+    int vt = 0, vp = 0, Ft = 0, Fp = 0;
+    for (int q = q0; q < q1; ++q) {
+      const uint32_t e = tile[tslot(line, s, q)];
+      if (e == kTileInf) continue;
+      const int fq = (int)e;
+      const int Fq = fq + q * q;
+      while (k >= 1) {
+        if ((long long)(Fq - Ft) * (vt - vp) <= (long long)(Ft - Fp) * (q - vt)) {
+          --k;
+          vt = vp;
+          Ft = Fp;
+          if (k >= 1) {
+            const uint32_t se = tile[tslot(line, s, q0 + k - 1)];
+            vp = (int)(se & 1023u);
+            Fp = (int)(se >> 10) + vp * vp;
+          }
+        } else {
+          break;
+        }
+      }
+      ++k;
+      tile[tslot(line, s, q0 + k)] = ((uint32_t)fq << 10) | (uint32_t)q;
+      vp = vt;
+      Fp = Ft;
+      vt = q;
+      Ft = Fq;
+    }
+  }
+  segs[line].lo[s] = 0;
+  segs[line].hi[s] = k + 1;
+  __syncthreads();
+  // ---- merges: (0,1) and (2,3), then (01, 23) ----
+  if (act && (s == 0 || s == 2)) merge_runs(tile, line, B, segs[line], s, s, s + 1);
+  __syncthreads();
+  if (act && s == 0) merge_runs(tile, line, B, segs[line], 0, 1, 3);
+  __syncthreads();
+  if (!act) return;
+  const SegLine S = segs[line];
+  int total = 0;
+#pragma unroll
+  for (int t = 0; t < KSEG; ++t) total += S.hi[t] - S.lo[t];
+  TOut *dst = dst_base + line;
+  if (total == 0) {
+    for (int q = q0; q < q1; ++q) store_dist<TOut>(dst + (int64_t)q * stride, -1);
+    return;
+  }
+  if (q0 >= q1) return;
+  // rank -> (segment, index)
+  auto at_rank = [&](int r, int &sg, int &ix) {
+#pragma unroll
+    for (int t = 0; t < KSEG; ++t) {
+      const int sz = S.hi[t] - S.lo[t];
+      if (r < sz) {
+        sg = t;
+        ix = S.lo[t] + r;
+        return;
+      }
+      r -= sz;
+    }
+    sg = KSEG - 1;
+    ix = S.hi[KSEG - 1] - 1;
+  };
+  // largest r with r == 0 or s(e_{r-1}, e_r) < q0
+  int lo = 0, hi = total - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    int sa, ia, sb, ib;
+    at_rank(mid - 1, sa, ia);
+    at_rank(mid, sb, ib);
+    if (boundary_lt(elem_at(tile, line, B, sa, ia), elem_at(tile, line, B, sb, ib), q0))
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  int cs, ci;
+  at_rank(lo, cs, ci);
+  Elem cur = elem_at(tile, line, B, cs, ci);
+  int ns = -1, ni = 0;
+  Elem nxt{0, 0, 0};
+  bool has_next = next_elem(S, cs, ci, KSEG - 1, ns, ni);
+  if (has_next) nxt = elem_at(tile, line, B, ns, ni);
+  for (int q = q0; q < q1; ++q) {
+    while (has_next && boundary_lt(cur, nxt, q)) {
+      cur = nxt;
+      cs = ns;
+      ci = ni;
+      has_next = next_elem(S, cs, ci, KSEG - 1, ns, ni);
+      if (has_next) nxt = elem_at(tile, line, B, ns, ni);
+    }
+    const int d = q - cur.v;
+    store_dist<TOut>(dst + (int64_t)q * stride, d * d + cur.f);
+  }
+}
+
+// Pass Z+Y fused: CTA = (z chunk, x).  The tile row y holds dz(x, y, z)^2 for
+// the 32 z of the chunk, computed from the packed occupancy words of line
+// (x, y) with a warp scan (no z-pass intermediate); the FH then runs along y.
+// Output: int32 g(x, y, z) = min over y' of (y - y')^2 + dz^2 (INT_MAX = none).
+__global__ void __launch_bounds__(ETHREADS) edt_zy_kernel(const uint32_t *__restrict__ bits, int64_t gy,
+                                                          int64_t words_z, int64_t lo0, int64_t lo1, int lo2,
+                                                          int n1, int n2, int32_t *__restrict__ out) {
+  extern __shared__ uint32_t smem[];
+  uint32_t *tile = smem;                                            // [n1][32]
+  SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)n1 * 32);  // [32]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int zc = blockIdx.x;
+  const int64_t x = blockIdx.y;
+  const int nw = (n2 + 31) >> 5;
+  const int nlines = min(32, n2 - zc * 32);
+  const uint32_t le_mask = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+  const uint32_t ge_mask = 0xffffffffu << lane;
+  for (int y = warp; y < n1; y += KSEG) {
+    const uint32_t *w = bits + ((lo0 + x) * gy + (lo1 + y)) * words_z;
+    uint32_t word = 0;
+    if (lane < nw) {
+      const int zb = lo2 + 32 * lane;
+      const int wi = zb >> 5, sh = zb & 31;
+      const uint32_t a = __ldg(w + wi);
+      const uint32_t b = (sh != 0 && wi + 1 < words_z) ? __ldg(w + wi + 1) : 0u;
+      word = sh ? __funnelshift_r(a, b, sh) : a;
+      const int valid = n2 - 32 * lane;
+      if (valid < 32) word &= (1u << valid) - 1u;
+    }
+    int last = word ? 32 * lane + 31 - __clz(word) : -1;
+    int first = word ? 32 * lane + __ffs(word) - 1 : 0x7fffffff;
+    if (nw > 1) {
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int l = __shfl_up_sync(kFull, last, d);
+        if (lane >= d) last = max(last, l);
+        const int f = __shfl_down_sync(kFull, first, d);
+        if (lane + d < 32) first = min(first, f);
+      }
+    }
+    int last_ex = __shfl_sync(kFull, last, (zc + 31) & 31);
+    if (zc == 0) last_ex = -1;
+    int first_ex = __shfl_sync(kFull, first, (zc + 1) & 31);
+    if (zc + 1 >= nw) first_ex = 0x7fffffff;
+    const uint32_t wc = __shfl_sync(kFull, word, zc);
+    const int z = 32 * zc + lane;
+    const uint32_t le = wc & le_mask, ge = wc & ge_mask;
+    const int left = le ? 32 * zc + 31 - __clz(le) : last_ex;
+    const int right = ge ? 32 * zc + __ffs(ge) - 1 : first_ex;
+    int d = 0x7fffffff;
+    if (left >= 0) d = z - left;
+    if (right != 0x7fffffff) d = min(d, right - z);
+    tile[tslot(lane, y / ((n1 + KSEG - 1) / KSEG), y)] =
+        (lane < nlines && d != 0x7fffffff) ? (uint32_t)(d * d) : kTileInf;
+  }
+  __syncthreads();
+  int32_t *dst = out + (x * n1) * (int64_t)n2 + zc * 32;
+  segmented_fh<int32_t>(tile, segs, n1, nlines, dst, n2);
+}
+
+// Pass X: CTA = (z chunk, y); rows x of the tile are the 32 z values of
+// g(x, y, zchunk) (one coalesced 128 B row each).
+__global__ void __launch_bounds__(ETHREADS) edt_x_kernel(const int32_t *__restrict__ g, int n0, int n1, int n2,
+                                                         float *__restrict__ out) {
+  extern __shared__ uint32_t smem[];
+  uint32_t *tile = smem;                                            // [n0][32]
+  SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)n0 * 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int zc = blockIdx.x;
+  const int64_t y = blockIdx.y;
+  const int nlines = min(32, n2 - zc * 32);
+  const int B = (n0 + KSEG - 1) / KSEG;
+  const int64_t row_stride = (int64_t)n1 * n2;
+  const int32_t *src = g + y * n2 + zc * 32 + lane;
+  int xr = warp;
+  for (; xr + 3 * KSEG < n0; xr += 4 * KSEG) {
+    int32_t v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) v[t] = lane < nlines ? src[(int64_t)(xr + t * KSEG) * row_stride] : kNoSrc32;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int xx = xr + t * KSEG;
+      tile[tslot(lane, xx / B, xx)] = v[t] == kNoSrc32 ? kTileInf : (uint32_t)v[t];
+    }
+  }
+  for (; xr < n0; xr += KSEG) {
+    const int32_t v = lane < nlines ? src[(int64_t)xr * row_stride] : kNoSrc32;
+    tile[tslot(lane, xr / B, xr)] = v == kNoSrc32 ? kTileInf : (uint32_t)v;
+  }
+  __syncthreads();
+  float *dst = out + y * n2 + zc * 32;
+  segmented_fh<float>(tile, segs, n0, nlines, dst, row_stride);
+}
+
 template <typename TIn, typename TOut>
 static int launch_fh(const TIn *in, TOut *out, int64_t n_outer, int64_t outer_stride, int64_t n2, int64_t len,
                      int64_t stride, int64_t max_dim, cudaStream_t s) {
@@ -487,29 +825,40 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], dou
   uint16_t *dz = reinterpret_cast<uint16_t *>(workspace);
   int32_t *g2 = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(workspace) + align_up(vox * 2, 256));
   const int64_t lines_z = n[0] * n[1];
+  const int64_t maxd = n[0] > n[1] ? (n[0] > n[2] ? n[0] : n[2]) : (n[1] > n[2] ? n[1] : n[2]);
+  int rc;
+  if (maxd <= 1024 && use_bits && n[0] <= 65535 && n[1] <= 65535) {
+    VPB_REQUIRE(grid->occ_bits, "use_bits set but grid->occ_bits is null");
+    // Pass Z+Y fused from the occupancy words, then pass X.
+    const size_t smem_zy = (size_t)n[1] * 32 * 4 + sizeof(SegLine) * 32;
+    const size_t smem_x = (size_t)n[0] * 32 * 4 + sizeof(SegLine) * 32;
+    if (smem_zy > 48 * 1024)
+      VPB_CUDA(cudaFuncSetAttribute(edt_zy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
+    if (smem_x > 48 * 1024)
+      VPB_CUDA(cudaFuncSetAttribute(edt_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
+    const unsigned zch = (unsigned)((n[2] + 31) / 32);
+    edt_zy_kernel<<<dim3(zch, (unsigned)n[0]), ETHREADS, smem_zy, s>>>(
+        grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], (int)lo[2], (int)n[1], (int)n[2],
+        g2);
+    rc = check_launch("edt_zy_kernel");
+    if (rc) return rc;
+    edt_x_kernel<<<dim3(zch, (unsigned)n[1]), ETHREADS, smem_x, s>>>(g2, (int)n[0], (int)n[1], (int)n[2], out_sq);
+    return check_launch("edt_x_kernel");
+  }
   if (use_bits) {
     VPB_REQUIRE(grid->occ_bits, "use_bits set but grid->occ_bits is null");
-    if (n[2] <= 1024) {
-      edt_pass_z_scan<<<dim3((unsigned)ceil_div(n[1], 8), (unsigned)n[0]), 256, 0, s>>>(grid->occ_bits, grid->dims[1],
-                                                                     ceil_div(grid->dims[2], 32), lo[0], lo[1],
-                                                                     (int)lo[2], n[0], n[1], (int)n[2], dz);
-    } else {
-      edt_pass_z_bits<<<(unsigned)ceil_div(lines_z, 8), 256, 0, s>>>(
-          grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], lo[2], n[0], n[1], n[2], dz);
-    }
+    edt_pass_z_bits<<<(unsigned)ceil_div(lines_z, 8), 256, 0, s>>>(
+        grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], lo[2], n[0], n[1], n[2], dz);
   } else {
     VPB_REQUIRE(grid->log_odds, "log_odds is null");
     edt_pass_z_logodds<<<(unsigned)ceil_div(lines_z, 8), 256, 0, s>>>(
         grid->log_odds, grid->dims[1], grid->dims[2], lo[0], lo[1], lo[2], n[0], n[1], n[2], thr, dz);
   }
-  int rc = check_launch("edt_pass_z");
+  rc = check_launch("edt_pass_z");
   if (rc) return rc;
-  const int64_t maxd = n[0] > n[1] ? (n[0] > n[2] ? n[0] : n[2]) : (n[1] > n[2] ? n[1] : n[2]);
   if (maxd <= 1024) {
-    // Pass Y: lines (x, z), element y at stride n2, outer stride n1*n2.
     rc = launch_fh_smem<uint16_t, int32_t>(dz, g2, n[0], n[1] * n[2], n[2], n[1], n[2], s);
     if (rc) return rc;
-    // Pass X: lines (y, z), element x at stride n1*n2, outer stride n2.
     return launch_fh_smem<int32_t, float>(g2, out_sq, n[1], n[2], n[2], n[0], n[1] * n[2], s);
   }
   rc = launch_fh<uint16_t, int32_t>(dz, g2, n[0], n[1] * n[2], n[2], n[1], n[2], maxd, s);

@@ -34,7 +34,8 @@ struct FusionArgs {
   int n_mask;
   double aabb_lo[3], aabb_hi[3];
   // fp32 prefilter constants
-  float of0, of1, of2, oabs, voxf, rf[9], tf[3], tabs, fxf, fyf, cxf, cyf, wf, hf;
+  float of0, of1, of2, oabs, azmax, voxf, rf[9], tf[3], tabs, fxf, fyf, cxh, cyh, ku, kv, au, av, wf, hf;
+  int usable;  // pixel_masked carries bit1 = usable return (vpb_update_occupancy)
   float bb_lo[3], bb_hi[3];
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr2[VPB_MAX_MASK_SPHERES];
@@ -44,145 +45,137 @@ __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a,
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
-// grid: x = lo0 + blockIdx.y ... flattened: blockIdx.x over (i0, i1, zword)
-__global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ FusionArgs A) {
-  const int lane = threadIdx.x & 31;
-  // grid: (ceil(n1 * wz_count / 8), n0); 32-bit index math only
-  const int per_x = (int)(A.n1 * A.wz_count);
-  const int w = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= per_x) return;
-  const int64_t i0 = blockIdx.y;
-  const int i1 = w / (int)A.wz_count;
-  const int64_t wz = A.wz_begin + (w - i1 * (int)A.wz_count);
-  const int64_t x = A.lo0 + i0, y = A.lo1 + i1;
-  const int64_t z = wz * 32 + lane;
-  const bool in_box = (z >= A.lo2) && (z < A.lo2 + A.n2);
-  const int64_t g = (x * A.gy + y) * A.gz + z;
-
-  bool touched = false;  // this lane's log-odds changed / was written
-  double newval = 0.0;
-
-  if (in_box) {
-    // ---- conservative fp32 prefilter ---------------------------------------
-    // Decides, with explicit error bounds, the voxels whose reference result
-    // is certainly "skip" (behind the camera, outside the image, or landing on
-    // a pixel without a usable return).  Everything else -- robot-mask
-    // candidates, pixel-boundary ambiguities, voxels that fuse -- takes the
-    // exact fp64 path below, so the result is bitwise the reference's.
-    const float axf = ((float)x + 0.5f) * A.voxf, ayf = ((float)y + 0.5f) * A.voxf, azf = ((float)z + 0.5f) * A.voxf;
-    const float pxf = A.of0 + axf;
-    const float pyf = A.of1 + ayf;
-    const float pzf = A.of2 + azf;
-    bool exact = false;
-    if (A.n_mask > 0 && pxf >= A.bb_lo[0] && pxf <= A.bb_hi[0] && pyf >= A.bb_lo[1] && pyf <= A.bb_hi[1] &&
-        pzf >= A.bb_lo[2] && pzf <= A.bb_hi[2])
-      exact = true;  // possibly inside a mask sphere
-    if (!exact) {
-      const float qxf = fmaf(A.rf[0], pxf, fmaf(A.rf[1], pyf, fmaf(A.rf[2], pzf, A.tf[0])));
-      const float qyf = fmaf(A.rf[3], pxf, fmaf(A.rf[4], pyf, fmaf(A.rf[5], pzf, A.tf[1])));
-      const float qzf = fmaf(A.rf[6], pxf, fmaf(A.rf[7], pyf, fmaf(A.rf[8], pzf, A.tf[2])));
-      // |q_f - q| <= dq: each centre coordinate is off by <= 2e-7 (|origin| +
-      // |(i + 1/2) voxel|) (no cancellation assumed), rotation entries are <= 1
-      // and the three FMAs add <= 2e-7 of the row magnitude: 4e-7 in total,
-      // taken with a 2.5x margin.
-      const float dq = 1e-6f * (A.oabs + fabsf(axf) + fabsf(ayf) + fabsf(azf) + A.tabs) + 1e-12f;
-      if (qzf < -dq) {
-        // qz <= 0 for sure: the reference skips this voxel
-      } else if (qzf <= dq + 1e-30f) {
-        exact = true;
-      } else {
-        const float iz = 1.0f / qzf;
-        const float ue = fmaf(A.fxf * qxf, iz, A.cxf) + 0.5f;
-        const float ve = fmaf(A.fyf * qyf, iz, A.cyf) + 0.5f;
-        const float den = qzf * (qzf - dq);
-        const float du = 2.0f * A.fxf * dq * (fabsf(qxf) + qzf) / den + 1e-6f * (fabsf(ue) + fabsf(A.cxf)) + 1e-5f;
-        const float dv = 2.0f * A.fyf * dq * (fabsf(qyf) + qzf) / den + 1e-6f * (fabsf(ve) + fabsf(A.cyf)) + 1e-5f;
-        const bool out_u = (ue < -du) || (ue >= A.wf + du);
-        const bool out_v = (ve < -dv) || (ve >= A.hf + dv);
-        if (!(out_u || out_v)) {
-          const float fu = floorf(ue), fv = floorf(ve);
-          const bool amb = (ue - fu <= du) || (fu + 1.0f - ue <= du) || (ve - fv <= dv) || (fv + 1.0f - ve <= dv) ||
-                           fu < 0.0f || fu >= A.wf || fv < 0.0f || fv >= A.hf;
-          if (amb) {
-            exact = true;
-          } else {
-            const int64_t pix = (int64_t)fv * A.width + (int64_t)fu;
-            const double measured = __ldg(A.depth + pix);
-            exact = measured >= A.d_min && measured <= A.d_max && !__ldg(A.pixel_masked + pix);
-          }
-        }
-        // else: certainly outside the image -> skip
-      }
-    }
-
-    if (exact) {
-      // ---- exact fp64 path: the reference's operations in its order ------
-      const double px = dadd(A.origin0, dmul(dadd((double)x, 0.5), A.voxel));
-      const double py = dadd(A.origin1, dmul(dadd((double)y, 0.5), A.voxel));
-      const double pz = dadd(A.origin2, dmul(dadd((double)z, 0.5), A.voxel));
-      // Robot mask (vp/mapping.py:310-325), exact strict-< test.
-      bool masked = false;
-      if (A.n_mask > 0 && px >= A.aabb_lo[0] && px <= A.aabb_hi[0] && py >= A.aabb_lo[1] &&
-          py <= A.aabb_hi[1] && pz >= A.aabb_lo[2] && pz <= A.aabb_hi[2]) {
-        for (int s = 0; s < A.n_mask; ++s) {
-          const double dx = dsub(px, A.mc[3 * s + 0]);
-          const double dy = dsub(py, A.mc[3 * s + 1]);
-          const double dz = dsub(pz, A.mc[3 * s + 2]);
-          const double d2 = dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
-          if (d2 < A.mr2[s]) {
-            masked = true;
-            break;
-          }
-        }
-      }
-      if (masked) {
+// Exact fp64 restatement of one voxel's update (vp/mapping.py:300-354), the
+// reference's operations in its order.  Returns true if the voxel was
+// written; *newval receives its log-odds.  Kept out of line so the fp32
+// prefilter loop stays small.
+__device__ __noinline__ bool exact_voxel(const FusionArgs &A, int64_t x, int64_t y, int64_t z, int64_t g,
+                                         double *newval) {
+  const double px = dadd(A.origin0, dmul(dadd((double)x, 0.5), A.voxel));
+  const double py = dadd(A.origin1, dmul(dadd((double)y, 0.5), A.voxel));
+  const double pz = dadd(A.origin2, dmul(dadd((double)z, 0.5), A.voxel));
+  // Robot mask (vp/mapping.py:310-325), exact strict-< test.
+  if (A.n_mask > 0 && px >= A.aabb_lo[0] && px <= A.aabb_hi[0] && py >= A.aabb_lo[1] && py <= A.aabb_hi[1] &&
+      pz >= A.aabb_lo[2] && pz <= A.aabb_hi[2]) {
+    for (int s = 0; s < A.n_mask; ++s) {
+      const double dx = dsub(px, A.mc[3 * s + 0]);
+      const double dy = dsub(py, A.mc[3 * s + 1]);
+      const double dz = dsub(pz, A.mc[3 * s + 2]);
+      const double d2 = dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz));
+      if (d2 < A.mr2[s]) {
         const double old = A.log_odds[g];
-        newval = old > 0.0 ? 0.0 : old;
+        *newval = old > 0.0 ? 0.0 : old;
         if (old > 0.0) A.log_odds[g] = 0.0;
         A.observed[g] = 1;
-        touched = true;
-      } else {
-        // Camera transform (vp/mapping.py:327-329): ((r0 px + r1 py) + r2 pz) + t
-        const double qx = dadd(dadd(dadd(dmul(A.r[0], px), dmul(A.r[1], py)), dmul(A.r[2], pz)), A.t[0]);
-        const double qy = dadd(dadd(dadd(dmul(A.r[3], px), dmul(A.r[4], py)), dmul(A.r[5], pz)), A.t[1]);
-        const double qz = dadd(dadd(dadd(dmul(A.r[6], px), dmul(A.r[7], py)), dmul(A.r[8], pz)), A.t[2]);
-        if (qz > 0.0) {
-          // u = fx * qx / qz + cx ; nearest pixel floor(u + 0.5) (:332-335)
-          const double u = dadd(__ddiv_rn(dmul(A.fx, qx), qz), A.cx);
-          const double v = dadd(__ddiv_rn(dmul(A.fy, qy), qz), A.cy);
-          const double uf = floor(dadd(u, 0.5));
-          const double vf = floor(dadd(v, 0.5));
-          if (uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height) {
-            const int64_t pix = (int64_t)vf * A.width + (int64_t)uf;
-            const double measured = __ldg(A.depth + pix);
-            if (measured >= A.d_min && measured <= A.d_max && !__ldg(A.pixel_masked + pix)) {
-              const double diff = dsub(qz, measured);
-              int cls = 0;
-              if (fabs(diff) <= A.tau) cls = 1;                    // hit
-              else if (qz < dsub(measured, A.tau)) cls = 2;        // miss
-              if (cls) {
-                double value = dadd(A.log_odds[g], cls == 1 ? A.l_hit : A.l_miss);
-                if (value < A.l_min) value = A.l_min;
-                else if (value > A.l_max) value = A.l_max;
-                A.log_odds[g] = value;
-                A.observed[g] = 1;
-                newval = value;
-                touched = true;
-              }
-            }
-          }
-        }
+        return true;
       }
     }
   }
+  // Camera transform (vp/mapping.py:327-329): ((r0 px + r1 py) + r2 pz) + t
+  const double qx = dadd(dadd(dadd(dmul(A.r[0], px), dmul(A.r[1], py)), dmul(A.r[2], pz)), A.t[0]);
+  const double qy = dadd(dadd(dadd(dmul(A.r[3], px), dmul(A.r[4], py)), dmul(A.r[5], pz)), A.t[1]);
+  const double qz = dadd(dadd(dadd(dmul(A.r[6], px), dmul(A.r[7], py)), dmul(A.r[8], pz)), A.t[2]);
+  if (!(qz > 0.0)) return false;
+  // u = fx * qx / qz + cx ; nearest pixel floor(u + 0.5) (:332-335)
+  const double u = dadd(__ddiv_rn(dmul(A.fx, qx), qz), A.cx);
+  const double v = dadd(__ddiv_rn(dmul(A.fy, qy), qz), A.cy);
+  const double uf = floor(dadd(u, 0.5));
+  const double vf = floor(dadd(v, 0.5));
+  if (!(uf >= 0.0 && uf < (double)A.width && vf >= 0.0 && vf < (double)A.height)) return false;
+  const int64_t pix = (int64_t)vf * A.width + (int64_t)uf;
+  const double measured = __ldg(A.depth + pix);
+  if (!(measured >= A.d_min && measured <= A.d_max) || (__ldg(A.pixel_masked + pix) & 1)) return false;
+  int cls = 0;
+  if (fabs(dsub(qz, measured)) <= A.tau) cls = 1;       // hit
+  else if (qz < dsub(measured, A.tau)) cls = 2;          // miss
+  if (!cls) return false;                                // occluded
+  double value = dadd(A.log_odds[g], cls == 1 ? A.l_hit : A.l_miss);
+  if (value < A.l_min) value = A.l_min;
+  else if (value > A.l_max) value = A.l_max;
+  A.log_odds[g] = value;
+  A.observed[g] = 1;
+  *newval = value;
+  return true;
+}
 
-  if (A.occ_bits != nullptr) {
-    const unsigned touched_mask = __ballot_sync(kFull, touched);
-    if (touched_mask != 0u) {
-      const unsigned occ_mask = __ballot_sync(kFull, touched && newval >= A.l_thr);
-      if (lane == 0) {
-        uint32_t *w = A.occ_bits + (x * A.gy + y) * A.words_z + wz;
-        *w = (*w & ~touched_mask) | (occ_mask & touched_mask);
+// One warp per (x, y) line of the box, looping over its z words.
+// grid: (ceil(n1 / 8), n0), 256 threads.
+__global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ FusionArgs A) {
+  const int lane = threadIdx.x & 31;
+  const int yi = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (yi >= A.n1) return;
+  const int64_t x = A.lo0 + blockIdx.y, y = A.lo1 + yi;
+  // ---- line constants of the conservative fp32 prefilter ----
+  // Decides, with explicit error bounds, the voxels whose reference result
+  // is certainly "skip" (behind the camera, outside the image, or landing on
+  // a pixel without a usable return).  Everything else -- robot-mask
+  // candidates, pixel-boundary ambiguities, voxels that fuse -- takes the
+  // exact fp64 path, so the result is bitwise the reference's.
+  const float axf = ((float)x + 0.5f) * A.voxf, ayf = ((float)y + 0.5f) * A.voxf;
+  const float pxf = A.of0 + axf, pyf = A.of1 + ayf;
+  const float qx0 = fmaf(A.rf[0], pxf, fmaf(A.rf[1], pyf, A.tf[0]));
+  const float qy0 = fmaf(A.rf[3], pxf, fmaf(A.rf[4], pyf, A.tf[1]));
+  const float qz0 = fmaf(A.rf[6], pxf, fmaf(A.rf[7], pyf, A.tf[2]));
+  // |q_f - q| <= dq: each centre coordinate is off by <= 2e-7 (|origin| +
+  // |(i + 1/2) voxel|), rotation entries are <= 1 and the three FMAs add
+  // <= 2e-7 of the row magnitude: 4e-7 in total, taken with a 2.5x margin.
+  const float dq = 1e-6f * (A.oabs + fabsf(axf) + fabsf(ayf) + A.azmax + A.tabs) + 1e-12f;
+  const bool line_mask = A.n_mask > 0 && pxf >= A.bb_lo[0] && pxf <= A.bb_hi[0] && pyf >= A.bb_lo[1] &&
+                         pyf <= A.bb_hi[1];
+  const int64_t gline = (x * A.gy + y) * A.gz;
+  for (int64_t wz = A.wz_begin; wz < A.wz_begin + A.wz_count; ++wz) {
+    const int64_t z = wz * 32 + lane;
+    const bool in_box = (z >= A.lo2) && (z < A.lo2 + A.n2);
+    bool exact = false;
+    if (in_box) {
+      const float pzf = A.of2 + ((float)z + 0.5f) * A.voxf;
+      if (line_mask && pzf >= A.bb_lo[2] && pzf <= A.bb_hi[2]) {
+        exact = true;  // possibly inside a mask sphere
+      } else {
+        const float qzf = fmaf(A.rf[8], pzf, qz0);
+        if (qzf < -dq) {
+          // qz <= 0 for sure: the reference skips this voxel
+        } else if (qzf <= 2.0f * dq + 1e-30f) {
+          exact = true;
+        } else {
+          const float qxf = fmaf(A.rf[2], pzf, qx0);
+          const float qyf = fmaf(A.rf[5], pzf, qy0);
+          const float iz = __fdividef(1.0f, qzf);  // <= 2 ulp, inside the margins below
+          const float ue = fmaf(A.fxf * qxf, iz, A.cxh);  // u + 1/2
+          const float ve = fmaf(A.fyf * qyf, iz, A.cyh);
+          // |d u / d q| <= fx (|qx| + qz) / (qz (qz - dq)) <= 8 fx (|qx_f| + qz_f + dq) / qz_f^2
+          // for qz_f > 2 dq; 10 fx taken.  Relative fp32 error of the
+          // projection itself <= 4 ulp: 1e-6 |u| + 1e-6 |c| + 4e-5.
+          const float iz2 = iz * iz;
+          const float du = A.ku * dq * (fabsf(qxf) + qzf + dq) * iz2 + 1e-6f * fabsf(ue) + A.au;
+          const float dv = A.kv * dq * (fabsf(qyf) + qzf + dq) * iz2 + 1e-6f * fabsf(ve) + A.av;
+          if (!(ue < -du || ue >= A.wf + du || ve < -dv || ve >= A.hf + dv)) {
+            const float fu = floorf(ue), fv = floorf(ve);
+            if ((ue - fu <= du) || (fu + 1.0f - ue <= du) || (ve - fv <= dv) || (fv + 1.0f - ve <= dv) ||
+                fu < 0.0f || fu >= A.wf || fv < 0.0f || fv >= A.hf) {
+              exact = true;  // pixel index not certain
+            } else {
+              const int pix = (int)fv * (int)A.width + (int)fu;
+              exact = A.usable ? (__ldg(A.pixel_masked + pix) == 2)
+                               : (__ldg(A.pixel_masked + pix) & 1) == 0 &&
+                                     __ldg(A.depth + pix) >= A.d_min && __ldg(A.depth + pix) <= A.d_max;
+            }
+          }
+          // else: certainly outside the image -> skip
+        }
+      }
+    }
+    bool touched = false;
+    double newval = 0.0;
+    if (exact) touched = exact_voxel(A, x, y, z, gline + z, &newval);
+    if (A.occ_bits != nullptr) {
+      const unsigned touched_mask = __ballot_sync(kFull, touched);
+      if (touched_mask != 0u) {
+        const unsigned occ_mask = __ballot_sync(kFull, touched && newval >= A.l_thr);
+        if (lane == 0) {
+          uint32_t *w = A.occ_bits + (x * A.gy + y) * A.words_z + wz;
+          *w = (*w & ~touched_mask) | (occ_mask & touched_mask);
+        }
       }
     }
   }
@@ -195,6 +188,7 @@ struct MaskPixArgs {
   double fx, fy, cx, cy, d_min, d_max;
   double r[9], t[3];
   int n_mask;
+  int encode_usable;  // out = 1 masked, 2 usable return, 0 otherwise
   double pad;
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr[VPB_MAX_MASK_SPHERES];
@@ -207,7 +201,8 @@ __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constan
   const int64_t vv = idx / A.width, uu = idx - vv * A.width;
   const double d = A.depth[idx];
   uint8_t inside = 0;
-  if (A.n_mask > 0 && d >= A.d_min && d <= A.d_max) {
+  const bool valid = d >= A.d_min && d <= A.d_max;
+  if (A.n_mask > 0 && valid) {
     const double z = d;
     const double xx = dmul(__ddiv_rn(dsub((double)uu, A.cx), A.fx), z);
     const double yy = dmul(__ddiv_rn(dsub((double)vv, A.cy), A.fy), z);
@@ -223,7 +218,7 @@ __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constan
       if (dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)) < dmul(r, r)) inside = 1;
     }
   }
-  A.out[idx] = inside;
+  A.out[idx] = A.encode_usable ? (inside ? 1 : (valid ? 2 : 0)) : inside;
 }
 
 // occupancy bits from log_odds: one warp per 32-voxel word.
@@ -279,8 +274,9 @@ int vpb_occ_bits_from_log_odds(const vpb_grid *grid, double thr, void *stream) {
   return check_launch("occ_bits_kernel");
 }
 
-int vpb_masked_pixels(const double *depth, const vpb_camera *cam, const double *centers,
-                      const double *radii, int64_t n_mask, double pad, uint8_t *out, void *stream) {
+static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const double *centers,
+                              const double *radii, int64_t n_mask, double pad, uint8_t *out, int encode,
+                              void *stream) {
   VPB_REQUIRE(depth && cam && out, "null argument to vpb_masked_pixels");
   MaskPixArgs A;
   memset(&A, 0, sizeof(A));
@@ -297,6 +293,7 @@ int vpb_masked_pixels(const double *depth, const vpb_camera *cam, const double *
   memcpy(A.r, cam->pose_r, sizeof(A.r));
   memcpy(A.t, cam->pose_t, sizeof(A.t));
   A.n_mask = (int)n_mask;
+  A.encode_usable = encode;
   A.pad = pad;
   const int64_t npx = cam->width * cam->height;
   if (npx == 0) return VPB_OK;
@@ -304,9 +301,9 @@ int vpb_masked_pixels(const double *depth, const vpb_camera *cam, const double *
   return check_launch("masked_pixels_kernel");
 }
 
-int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
-                    const double *depth, const uint8_t *pixel_masked, const double *centers,
-                    const double *radii, int64_t n_mask, const vpb_map_params *p, void *stream) {
+static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
+                     const double *depth, const uint8_t *pixel_masked, const double *centers,
+                     const double *radii, int64_t n_mask, const vpb_map_params *p, int usable, void *stream) {
   VPB_REQUIRE(grid && grid->log_odds && grid->observed && cam && depth && pixel_masked && p,
               "null argument to vpb_fuse_voxels");
   for (int k = 0; k < 3; ++k)
@@ -338,6 +335,7 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3
   A.tau = p->tau; A.l_hit = p->l_hit; A.l_miss = p->l_miss;
   A.l_min = p->l_min; A.l_max = p->l_max; A.l_thr = p->l_occ_threshold;
   A.n_mask = (int)n_mask;
+  A.usable = usable;
   A.of0 = (float)A.origin0;
   A.of1 = (float)A.origin1;
   A.of2 = (float)A.origin2;
@@ -355,25 +353,42 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3
   }
   A.fxf = (float)A.fx;
   A.fyf = (float)A.fy;
-  A.cxf = (float)A.cx;
-  A.cyf = (float)A.cy;
+  A.cxh = (float)(A.cx + 0.5);
+  A.cyh = (float)(A.cy + 0.5);
+  A.ku = 10.0f * fabsf(A.fxf);
+  A.kv = 10.0f * fabsf(A.fyf);
+  A.au = 1e-6f * fabsf(A.cxh) + 4e-5f;
+  A.av = 1e-6f * fabsf(A.cyh) + 4e-5f;
+  A.azmax = fmaxf(fabsf((float)((double)lo[2] + 0.5) * A.voxf), fabsf((float)((double)(lo[2] + n[2]) + 0.5) * A.voxf));
   A.wf = (float)A.width;
   A.hf = (float)A.height;
   // the fp32 prefilter assumes an orthonormal world->camera rotation and a
   // scene within float range; anything else simply takes the exact path
-  VPB_REQUIRE(A.n0 <= 65535 && A.n1 * A.wz_count < (1ll << 30), "box too large for the fusion grid");
-  dim3 launch_grid((unsigned)ceil_div(A.n1 * A.wz_count, 8), (unsigned)A.n0);
+  VPB_REQUIRE(A.n0 <= 65535, "box too large for the fusion grid");
+  dim3 launch_grid((unsigned)ceil_div(A.n1, 8), (unsigned)A.n0);
   fuse_kernel<<<launch_grid, 256, 0, as_stream(stream)>>>(A);
   return check_launch("fuse_kernel");
+}
+
+int vpb_masked_pixels(const double *depth, const vpb_camera *cam, const double *centers, const double *radii,
+                      int64_t n_mask, double pad, uint8_t *out, void *stream) {
+  return masked_pixels_impl(depth, cam, centers, radii, n_mask, pad, out, 0, stream);
+}
+
+int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
+                    const double *depth, const uint8_t *pixel_masked, const double *centers, const double *radii,
+                    int64_t n_mask, const vpb_map_params *p, void *stream) {
+  return fuse_impl(grid, lo, n, cam, depth, pixel_masked, centers, radii, n_mask, p, 0, stream);
 }
 
 int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
                          const double *depth, const double *centers, const double *radii, int64_t n_mask,
                          double mask_pad, const vpb_map_params *params, uint8_t *pixel_scratch, void *stream) {
   VPB_REQUIRE(pixel_scratch, "pixel scratch is null");
-  int rc = vpb_masked_pixels(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, stream);
+  // pixel classes in one byte: 1 = return on the robot body, 2 = usable return
+  int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, stream);
   if (rc) return rc;
-  return vpb_fuse_voxels(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, stream);
+  return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, stream);
 }
 
 }  // extern "C"

@@ -80,8 +80,8 @@ __device__ __forceinline__ void tsincos<double>(double x, double *s, double *c) 
 template <typename T>
 struct Query {
   T f0, f1, f2;
-  float v[8];
-  uint8_t cell;  // index of the containing cell among the corners
+  float v0, v1, v2, v3, v4, v5, v6, v7;  // corners (a/b along x, y, z)
+  float cell;                            // value of the containing cell
   bool outside;
 };
 
@@ -114,34 +114,35 @@ __device__ __forceinline__ void query_issue(const Prob<T> &P, T px, T py, T pz, 
   Q.f0 = c0 - T(a0);
   Q.f1 = c1 - T(a1);
   Q.f2 = c2 - T(a2);
-  Q.cell = (uint8_t)(((i0 == a0) ? 0 : 4) | ((i1 == a1) ? 0 : 2) | ((i2 == a2) ? 0 : 1));
   const float *sq = P.sq;
   const size_t r00 = ((size_t)a0 * n1 + a1) * n2, r01 = ((size_t)a0 * n1 + b1) * n2;
   const size_t r10 = ((size_t)b0 * n1 + a1) * n2, r11 = ((size_t)b0 * n1 + b1) * n2;
-  Q.v[0] = __ldg(sq + r00 + a2);
-  Q.v[1] = __ldg(sq + r00 + b2);
-  Q.v[2] = __ldg(sq + r01 + a2);
-  Q.v[3] = __ldg(sq + r01 + b2);
-  Q.v[4] = __ldg(sq + r10 + a2);
-  Q.v[5] = __ldg(sq + r10 + b2);
-  Q.v[6] = __ldg(sq + r11 + a2);
-  Q.v[7] = __ldg(sq + r11 + b2);
+  Q.v0 = __ldg(sq + r00 + a2);
+  Q.v1 = __ldg(sq + r00 + b2);
+  Q.v2 = __ldg(sq + r01 + a2);
+  Q.v3 = __ldg(sq + r01 + b2);
+  Q.v4 = __ldg(sq + r10 + a2);
+  Q.v5 = __ldg(sq + r10 + b2);
+  Q.v6 = __ldg(sq + r11 + a2);
+  Q.v7 = __ldg(sq + r11 + b2);
+  // containing cell = corner (i == a ? a : b) on every axis
+  const bool sx = i0 != a0, sy = i1 != a1, sz = i2 != a2;
+  const float e00 = sz ? Q.v1 : Q.v0, e01 = sz ? Q.v3 : Q.v2;
+  const float e10 = sz ? Q.v5 : Q.v4, e11 = sz ? Q.v7 : Q.v6;
+  const float e0 = sy ? e01 : e00, e1 = sy ? e11 : e10;
+  Q.cell = sx ? e1 : e0;
 }
 
 template <typename T>
 __device__ __forceinline__ T query_finish(const Prob<T> &P, const Query<T> &Q) {
   if (Q.outside) return P.outside;
-  float cell = Q.v[0];
-#pragma unroll
-  for (int c = 1; c < 8; ++c)
-    if (Q.cell == c) cell = Q.v[c];
-  if (cell == 0.0f) return T(0);
-  if (isinf(cell)) return (T)cell;  // no source in the volume: all values inf
+  if (Q.cell == 0.0f) return T(0);
+  if (isinf(Q.cell)) return (T)Q.cell;  // no source in the volume: all values inf
   const T e0 = T(1) - Q.f0, e1 = T(1) - Q.f1, e2 = T(1) - Q.f2;
-  const T c00 = (T)Q.v[0] * e0 + (T)Q.v[4] * Q.f0;
-  const T c01 = (T)Q.v[1] * e0 + (T)Q.v[5] * Q.f0;
-  const T c10 = (T)Q.v[2] * e0 + (T)Q.v[6] * Q.f0;
-  const T c11 = (T)Q.v[3] * e0 + (T)Q.v[7] * Q.f0;
+  const T c00 = (T)Q.v0 * e0 + (T)Q.v4 * Q.f0;
+  const T c01 = (T)Q.v1 * e0 + (T)Q.v5 * Q.f0;
+  const T c10 = (T)Q.v2 * e0 + (T)Q.v6 * Q.f0;
+  const T c11 = (T)Q.v3 * e0 + (T)Q.v7 * Q.f0;
   const T c0v = c00 * e1 + c10 * Q.f1;
   const T c1v = c01 * e1 + c11 * Q.f1;
   const T value = c0v * e2 + c1v * Q.f2;
