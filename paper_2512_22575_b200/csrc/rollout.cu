@@ -618,43 +618,60 @@ __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) smpc_kernel(
   }
   __syncthreads();
   // ---- CTA partial (fixed order over the NW candidates) ----
-  double mn = dinf();
-  int best = -1, nonfinite = 0;
+  double *wt_s = S.misc + 32;  // NW weights
+  if (threadIdx.x == 0) {
+    double mn = dinf();
+    int best = -1, nonfinite = 0;
 #pragma unroll
-  for (int w = 0; w < NW; ++w) {
-    if (cta_m0 + w >= io.M) continue;
-    const double c = tot[w];
-    if (!(c < dinf())) {
-      ++nonfinite;
-      continue;
+    for (int w = 0; w < NW; ++w) {
+      if (cta_m0 + w >= io.M) continue;
+      const double c = tot[w];
+      if (!(c < dinf())) {
+        ++nonfinite;
+        continue;
+      }
+      if (c < mn) {
+        mn = c;
+        best = w;
+      }
     }
-    if (c < mn) {
-      mn = c;
-      best = w;
-    }
+    S.misc[45] = mn;
+    S.misc[46] = (double)nonfinite;
+    S.misc[47] = best >= 0 ? (double)(io.m_offset + cta_m0 + best) : -1.0;
   }
-  double wt[NW];
-  double Zc = 0.0;
-#pragma unroll
-  for (int w = 0; w < NW; ++w) {
+  __syncthreads();
+  if (threadIdx.x < NW) {
+    const int w = threadIdx.x;
     const double c = tot[w];
     const bool ok = (cta_m0 + w < io.M) && (c < dinf());
-    wt[w] = ok ? exp(-(c - mn) / io.lam) : 0.0;
-    Zc += wt[w];
+    wt_s[w] = ok ? exp(-(c - S.misc[45]) / io.lam) : 0.0;
   }
+  __syncthreads();
   double *part = io.cta_parts + (size_t)blockIdx.x * Lp;
   if (threadIdx.x == 0) {
-    part[0] = mn;
-    part[1] = Zc;
-    part[2] = (double)nonfinite;
-    part[3] = best >= 0 ? (double)(io.m_offset + cta_m0 + best) : -1.0;
-  }
-  for (int e = threadIdx.x; e < hn; e += blockDim.x) {
-    double acc = 0.0;
+    double Zc = 0.0;
 #pragma unroll
-    for (int w = 0; w < NW; ++w)
-      if (wt[w] != 0.0) acc += wt[w] * load_e<ET>(eps + (size_t)(cta_m0 + w) * hn + e);
-    part[kPartHead + e] = acc;
+    for (int w = 0; w < NW; ++w) Zc += wt_s[w];
+    part[0] = S.misc[45];
+    part[1] = Zc;
+    part[2] = S.misc[46];
+    part[3] = S.misc[47];
+  }
+  {
+    double wt[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) wt[w] = wt_s[w];
+    for (int e = threadIdx.x; e < hn; e += blockDim.x) {
+      double ev[NW];
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+        ev[w] = (cta_m0 + w < io.M) ? load_e<ET>(eps + (size_t)(cta_m0 + w) * hn + e) : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int w = 0; w < NW; ++w)
+        if (wt[w] != 0.0) acc += wt[w] * ev[w];
+      part[kPartHead + e] = acc;
+    }
   }
   // ---- group merge by the group's last CTA ----
   __threadfence();

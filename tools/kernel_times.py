@@ -1,34 +1,35 @@
-"""Warm per-stage device timings (CUDA events, median of N) for the C2/C3
-scene: fusion, EDT, rollout (evaluate), fused SMPC step (partial only and
-full), M=1 evaluate, sampler.  Prints one JSON object."""
+"""Warm per-kernel device durations (CUPTI via torch.profiler) for the C2/C3
+scene: fusion, EDT, sampler, rollout, fused SMPC step, graph replay.
+Host launch overhead is excluded (kernel durations only).  Prints JSON."""
 
 import argparse
 import json
-import statistics
 import sys
+from collections import defaultdict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
 
-def timeit(fn, n=30, warm=5):
+def kernel_times(fn, n=20, warm=5):
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
-    ts = []
-    for _ in range(n):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
-        fn()
-        b.record()
-        b.synchronize()
-        ts.append(a.elapsed_time(b) * 1e3)
-    return statistics.median(ts)
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(n):
+            fn()
+        torch.cuda.synchronize()
+    acc = defaultdict(float)
+    cnt = defaultdict(int)
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA and e.device_time_total > 0:
+            acc[e.name[:60]] += e.device_time_total
+            cnt[e.name[:60]] += 1
+    return {k: round(v / n, 2) for k, v in acc.items()}
 
 
 def main():
@@ -47,18 +48,17 @@ def main():
     nom = torch.zeros((a.horizon, 7), dtype=torch.float64, device="cuda")
     eps = pl.sample_device(3)
     one = torch.zeros((1, a.horizon, 7), dtype=torch.float64, device="cuda")
-    out = {}
-    out["fusion_us"] = timeit(lambda: mapper.update(S["depth"], mask=mask))
-    out["edt_us"] = timeit(lambda: mapper.recompute_edt())
-    out["sampler_us"] = timeit(lambda: pl.sample_device(3, out=eps))
-    out["rollout_eval_us"] = timeit(lambda: pl.evaluate_device(st, goal, field, eps, nom))
-    out["smpc_partial_us"] = timeit(lambda: pl.smpc_partial_device(st, goal, field, nom, eps))
-    out["smpc_step_us"] = timeit(lambda: pl.smpc_step_device(st, goal, field, nom, eps))
-    out["eval_M1_us"] = timeit(lambda: pl.evaluate_device(st, goal, field, one))
+    out = {
+        "fusion": kernel_times(lambda: mapper.update(S["depth"], mask=mask)),
+        "edt": kernel_times(lambda: mapper.recompute_edt()),
+        "rollout_eval": kernel_times(lambda: pl.evaluate_device(st, goal, field, eps, nom)),
+        "smpc_step": kernel_times(lambda: pl.smpc_step_device(st, goal, field, nom, eps)),
+        "eval_M1": kernel_times(lambda: pl.evaluate_device(st, goal, field, one)),
+    }
     g = PL.SmpcGraph(pl, field)
     g.stage(st, goal, None, 0)
-    out["graph_step_us"] = timeit(g.replay)
-    print(json.dumps({k: round(v, 2) for k, v in out.items()}))
+    out["graph_replay"] = kernel_times(g.replay)
+    print(json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":
