@@ -478,14 +478,19 @@ __device__ __forceinline__ Elem elem_at(const uint32_t *tile, int line, int B, i
   return r;
 }
 
-// s(a, b) < q  <=>  F_b - F_a < 2 q (v_b - v_a)
+// s(a, b) < q  <=>  F_b - F_a < 2 q (v_b - v_a).  WIDE: 64-bit products
+// (lines longer than 512, where 3 (n-1)^3 can exceed 2^31).
+template <bool WIDE>
 __device__ __forceinline__ bool boundary_lt(const Elem &a, const Elem &b, int q) {
-  return (long long)(b.F - a.F) < 2ll * q * (b.v - a.v);
+  if constexpr (WIDE) return (long long)(b.F - a.F) < 2ll * q * (b.v - a.v);
+  else return (b.F - a.F) < 2 * q * (b.v - a.v);
 }
 
 // dominated(l, p, r): s(l, p) >= s(p, r)
+template <bool WIDE>
 __device__ __forceinline__ bool dominated(const Elem &l, const Elem &p, const Elem &r) {
-  return (long long)(p.F - l.F) * (r.v - p.v) >= (long long)(r.F - p.F) * (p.v - l.v);
+  if constexpr (WIDE) return (long long)(p.F - l.F) * (r.v - p.v) >= (long long)(r.F - p.F) * (p.v - l.v);
+  else return (p.F - l.F) * (r.v - p.v) >= (r.F - p.F) * (p.v - l.v);
 }
 
 // previous / next non-empty element in segment order
@@ -520,8 +525,8 @@ __device__ __forceinline__ bool next_elem(const SegLine &S, int seg, int idx, in
 }
 
 // Merge left run (segments a..b) with right run (b+1..c) of one line.
+template <bool WIDE>
 __device__ void merge_runs(const uint32_t *tile, int line, int B, SegLine &S, int a, int b, int c) {
-  // last element of the left run, first of the right run
   int ls = -1, li = 0, rs = -1, ri = 0;
   for (int t = b; t >= a; --t)
     if (S.hi[t] > S.lo[t]) {
@@ -543,7 +548,7 @@ __device__ void merge_runs(const uint32_t *tile, int line, int B, SegLine &S, in
     int ps, pi;
     if (prev_elem(S, ls, li, a, ps, pi)) {
       const Elem L2 = elem_at(tile, line, B, ps, pi);
-      if (dominated(L2, L1, R1)) {
+      if (dominated<WIDE>(L2, L1, R1)) {
         S.hi[ls] = li;  // drop the left run's last element
         ls = ps;
         li = pi;
@@ -554,7 +559,7 @@ __device__ void merge_runs(const uint32_t *tile, int line, int B, SegLine &S, in
       int ns, ni;
       if (next_elem(S, rs, ri, c, ns, ni)) {
         const Elem R2 = elem_at(tile, line, B, ns, ni);
-        if (dominated(L1, R1, R2)) {
+        if (dominated<WIDE>(L1, R1, R2)) {
           S.lo[rs] = ri + 1;  // drop the right run's first element
           rs = ns;
           ri = ni;
@@ -578,41 +583,43 @@ __device__ __forceinline__ void store_dist<float>(float *p, int v) {
 }
 
 // Envelope + output for the tile (called by all ETHREADS threads after the
-// tile is filled and synchronised).  dst(line) + q * stride receives output q.
-template <typename TOut>
+// tile is filled and synchronised).  dst_base + line + q * stride receives
+// output q of `line`.
+template <typename TOut, bool WIDE>
 __device__ void segmented_fh(uint32_t *tile, SegLine *segs, int len, int nlines_active, TOut *dst_base,
                              int64_t stride) {
   const int tid = threadIdx.x;
-  const int s = tid >> 5;          // segment = warp index
-  const int line = tid & 31;       // z lane
+  const int s = tid >> 5;     // segment = warp index
+  const int line = tid & 31;  // z lane
   const int B = (len + KSEG - 1) / KSEG;
   const int q0 = s * B, q1 = min(len, q0 + B);
   const bool act = line < nlines_active;
+  uint32_t *col = tile + ((line + 8 * s) & 31);  // this thread's column; row r at col[r * 32]
   // ---- forward sweep on this segment (stack in place) ----
   int k = -1;
   if (act) {
     int vt = 0, vp = 0, Ft = 0, Fp = 0;
-    for (int q = q0; q < q1; ++q) {
-      const uint32_t e = tile[tslot(line, s, q)];
+    const uint32_t *src = col + q0 * 32;
+    for (int q = q0; q < q1; ++q, src += 32) {
+      const uint32_t e = *src;
       if (e == kTileInf) continue;
       const int fq = (int)e;
       const int Fq = fq + q * q;
       while (k >= 1) {
-        if ((long long)(Fq - Ft) * (vt - vp) <= (long long)(Ft - Fp) * (q - vt)) {
-          --k;
-          vt = vp;
-          Ft = Fp;
-          if (k >= 1) {
-            const uint32_t se = tile[tslot(line, s, q0 + k - 1)];
-            vp = (int)(se & 1023u);
-            Fp = (int)(se >> 10) + vp * vp;
-          }
-        } else {
-          break;
+        const bool pop = WIDE ? ((long long)(Fq - Ft) * (vt - vp) <= (long long)(Ft - Fp) * (q - vt))
+                              : ((Fq - Ft) * (vt - vp) <= (Ft - Fp) * (q - vt));
+        if (!pop) break;
+        --k;
+        vt = vp;
+        Ft = Fp;
+        if (k >= 1) {
+          const uint32_t se = col[(q0 + k - 1) * 32];
+          vp = (int)(se & 1023u);
+          Fp = (int)(se >> 10) + vp * vp;
         }
       }
       ++k;
-      tile[tslot(line, s, q0 + k)] = ((uint32_t)fq << 10) | (uint32_t)q;
+      col[(q0 + k) * 32] = ((uint32_t)fq << 10) | (uint32_t)q;
       vp = vt;
       Fp = Ft;
       vt = q;
@@ -623,21 +630,20 @@ __device__ void segmented_fh(uint32_t *tile, SegLine *segs, int len, int nlines_
   segs[line].hi[s] = k + 1;
   __syncthreads();
   // ---- merges: (0,1) and (2,3), then (01, 23) ----
-  if (act && (s == 0 || s == 2)) merge_runs(tile, line, B, segs[line], s, s, s + 1);
+  if (act && (s == 0 || s == 2)) merge_runs<WIDE>(tile, line, B, segs[line], s, s, s + 1);
   __syncthreads();
-  if (act && s == 0) merge_runs(tile, line, B, segs[line], 0, 1, 3);
+  if (act && s == 0) merge_runs<WIDE>(tile, line, B, segs[line], 0, 1, 3);
   __syncthreads();
-  if (!act) return;
+  if (!act || q0 >= q1) return;
   const SegLine S = segs[line];
   int total = 0;
 #pragma unroll
   for (int t = 0; t < KSEG; ++t) total += S.hi[t] - S.lo[t];
-  TOut *dst = dst_base + line;
+  TOut *dst = dst_base + line + (int64_t)q0 * stride;
   if (total == 0) {
-    for (int q = q0; q < q1; ++q) store_dist<TOut>(dst + (int64_t)q * stride, -1);
+    for (int q = q0; q < q1; ++q, dst += stride) store_dist<TOut>(dst, -1);
     return;
   }
-  if (q0 >= q1) return;
   // rank -> (segment, index)
   auto at_rank = [&](int r, int &sg, int &ix) {
 #pragma unroll
@@ -660,7 +666,7 @@ __device__ void segmented_fh(uint32_t *tile, SegLine *segs, int len, int nlines_
     int sa, ia, sb, ib;
     at_rank(mid - 1, sa, ia);
     at_rank(mid, sb, ib);
-    if (boundary_lt(elem_at(tile, line, B, sa, ia), elem_at(tile, line, B, sb, ib), q0))
+    if (boundary_lt<WIDE>(elem_at(tile, line, B, sa, ia), elem_at(tile, line, B, sb, ib), q0))
       lo = mid;
     else
       hi = mid - 1;
@@ -672,8 +678,8 @@ __device__ void segmented_fh(uint32_t *tile, SegLine *segs, int len, int nlines_
   Elem nxt{0, 0, 0};
   bool has_next = next_elem(S, cs, ci, KSEG - 1, ns, ni);
   if (has_next) nxt = elem_at(tile, line, B, ns, ni);
-  for (int q = q0; q < q1; ++q) {
-    while (has_next && boundary_lt(cur, nxt, q)) {
+  for (int q = q0; q < q1; ++q, dst += stride) {
+    while (has_next && boundary_lt<WIDE>(cur, nxt, q)) {
       cur = nxt;
       cs = ns;
       ci = ni;
@@ -681,19 +687,22 @@ __device__ void segmented_fh(uint32_t *tile, SegLine *segs, int len, int nlines_
       if (has_next) nxt = elem_at(tile, line, B, ns, ni);
     }
     const int d = q - cur.v;
-    store_dist<TOut>(dst + (int64_t)q * stride, d * d + cur.f);
+    store_dist<TOut>(dst, d * d + cur.f);
   }
 }
 
 // Pass Z+Y fused: CTA = (z chunk, x).  The tile row y holds dz(x, y, z)^2 for
 // the 32 z of the chunk, computed from the packed occupancy words of line
-// (x, y) with a warp scan (no z-pass intermediate); the FH then runs along y.
+// (x, y): the word of the chunk gives the in-chunk neighbours, a ballot over
+// the line's non-empty words gives the nearest non-empty word on each side
+// (no z-pass intermediate).  The FH then runs along y.
 // Output: int32 g(x, y, z) = min over y' of (y - y')^2 + dz^2 (INT_MAX = none).
+template <bool WIDE>
 __global__ void __launch_bounds__(ETHREADS) edt_zy_kernel(const uint32_t *__restrict__ bits, int64_t gy,
                                                           int64_t words_z, int64_t lo0, int64_t lo1, int lo2,
                                                           int n1, int n2, int32_t *__restrict__ out) {
   extern __shared__ uint32_t smem[];
-  uint32_t *tile = smem;                                            // [n1][32]
+  uint32_t *tile = smem;                                                // [n1][32]
   SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)n1 * 32);  // [32]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int zc = blockIdx.x;
@@ -702,55 +711,52 @@ __global__ void __launch_bounds__(ETHREADS) edt_zy_kernel(const uint32_t *__rest
   const int nlines = min(32, n2 - zc * 32);
   const uint32_t le_mask = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
   const uint32_t ge_mask = 0xffffffffu << lane;
-  for (int y = warp; y < n1; y += KSEG) {
-    const uint32_t *w = bits + ((lo0 + x) * gy + (lo1 + y)) * words_z;
+  const uint32_t below_zc = zc == 0 ? 0u : (0xffffffffu >> (32 - zc));         // words < zc
+  const uint32_t above_zc = zc >= 31 ? 0u : (0xffffffffu << (zc + 1));          // words > zc
+  const int B = (n1 + KSEG - 1) / KSEG;
+  const int zb_lane = lo2 + 32 * lane;
+  const int wi_lane = zb_lane >> 5, sh_lane = zb_lane & 31;
+  const int valid_lane = n2 - 32 * lane;
+  const uint32_t *wbase = bits + ((lo0 + x) * gy + lo1) * words_z;
+  // warp w fills the rows of segment w (its rotated column is warp-uniform)
+  const int y0 = warp * B, y1 = min(n1, y0 + B);
+  for (int y = y0; y < y1; ++y) {
+    const uint32_t *w = wbase + (int64_t)y * words_z;
     uint32_t word = 0;
     if (lane < nw) {
-      const int zb = lo2 + 32 * lane;
-      const int wi = zb >> 5, sh = zb & 31;
-      const uint32_t a = __ldg(w + wi);
-      const uint32_t b = (sh != 0 && wi + 1 < words_z) ? __ldg(w + wi + 1) : 0u;
-      word = sh ? __funnelshift_r(a, b, sh) : a;
-      const int valid = n2 - 32 * lane;
-      if (valid < 32) word &= (1u << valid) - 1u;
+      const uint32_t a = __ldg(w + wi_lane);
+      const uint32_t b = (sh_lane != 0 && wi_lane + 1 < words_z) ? __ldg(w + wi_lane + 1) : 0u;
+      word = sh_lane ? __funnelshift_r(a, b, sh_lane) : a;
+      if (valid_lane < 32) word &= (1u << valid_lane) - 1u;
     }
-    int last = word ? 32 * lane + 31 - __clz(word) : -1;
-    int first = word ? 32 * lane + __ffs(word) - 1 : 0x7fffffff;
-    if (nw > 1) {
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int l = __shfl_up_sync(kFull, last, d);
-        if (lane >= d) last = max(last, l);
-        const int f = __shfl_down_sync(kFull, first, d);
-        if (lane + d < 32) first = min(first, f);
-      }
-    }
-    int last_ex = __shfl_sync(kFull, last, (zc + 31) & 31);
-    if (zc == 0) last_ex = -1;
-    int first_ex = __shfl_sync(kFull, first, (zc + 1) & 31);
-    if (zc + 1 >= nw) first_ex = 0x7fffffff;
+    const uint32_t nz = __ballot_sync(kFull, word != 0u);
     const uint32_t wc = __shfl_sync(kFull, word, zc);
+    const uint32_t lmask = nz & below_zc, rmask = nz & above_zc;
+    const int lw = lmask ? 31 - __clz(lmask) : 0;
+    const int rw = rmask ? __ffs(rmask) - 1 : 0;
+    const uint32_t lword = __shfl_sync(kFull, word, lw);
+    const uint32_t rword = __shfl_sync(kFull, word, rw);
     const int z = 32 * zc + lane;
     const uint32_t le = wc & le_mask, ge = wc & ge_mask;
-    const int left = le ? 32 * zc + 31 - __clz(le) : last_ex;
-    const int right = ge ? 32 * zc + __ffs(ge) - 1 : first_ex;
+    const int left = le ? 32 * zc + 31 - __clz(le) : (lmask ? 32 * lw + 31 - __clz(lword) : -1);
+    const int right = ge ? 32 * zc + __ffs(ge) - 1 : (rmask ? 32 * rw + __ffs(rword) - 1 : 0x7fffffff);
     int d = 0x7fffffff;
     if (left >= 0) d = z - left;
     if (right != 0x7fffffff) d = min(d, right - z);
-    tile[tslot(lane, y / ((n1 + KSEG - 1) / KSEG), y)] =
-        (lane < nlines && d != 0x7fffffff) ? (uint32_t)(d * d) : kTileInf;
+    tile[y * 32 + ((lane + 8 * warp) & 31)] = (lane < nlines && d != 0x7fffffff) ? (uint32_t)(d * d) : kTileInf;
   }
   __syncthreads();
   int32_t *dst = out + (x * n1) * (int64_t)n2 + zc * 32;
-  segmented_fh<int32_t>(tile, segs, n1, nlines, dst, n2);
+  segmented_fh<int32_t, WIDE>(tile, segs, n1, nlines, dst, n2);
 }
 
 // Pass X: CTA = (z chunk, y); rows x of the tile are the 32 z values of
 // g(x, y, zchunk) (one coalesced 128 B row each).
+template <bool WIDE>
 __global__ void __launch_bounds__(ETHREADS) edt_x_kernel(const int32_t *__restrict__ g, int n0, int n1, int n2,
                                                          float *__restrict__ out) {
   extern __shared__ uint32_t smem[];
-  uint32_t *tile = smem;                                            // [n0][32]
+  uint32_t *tile = smem;                                                // [n0][32]
   SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)n0 * 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int zc = blockIdx.x;
@@ -758,25 +764,26 @@ __global__ void __launch_bounds__(ETHREADS) edt_x_kernel(const int32_t *__restri
   const int nlines = min(32, n2 - zc * 32);
   const int B = (n0 + KSEG - 1) / KSEG;
   const int64_t row_stride = (int64_t)n1 * n2;
-  const int32_t *src = g + y * n2 + zc * 32 + lane;
-  int xr = warp;
-  for (; xr + 3 * KSEG < n0; xr += 4 * KSEG) {
+  const bool on = lane < nlines;
+  // warp w fills segment w's rows (so the rotated column is warp-uniform)
+  const int r0 = warp * B, r1 = min(n0, r0 + B);
+  const int32_t *src = g + y * n2 + zc * 32 + lane + (int64_t)r0 * row_stride;
+  uint32_t *dcol = tile + ((lane + 8 * warp) & 31);
+  int r = r0;
+  for (; r + 4 <= r1; r += 4, src += 4 * row_stride) {
     int32_t v[4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) v[t] = lane < nlines ? src[(int64_t)(xr + t * KSEG) * row_stride] : kNoSrc32;
+    for (int t = 0; t < 4; ++t) v[t] = on ? __ldg(src + t * row_stride) : kNoSrc32;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int xx = xr + t * KSEG;
-      tile[tslot(lane, xx / B, xx)] = v[t] == kNoSrc32 ? kTileInf : (uint32_t)v[t];
-    }
+    for (int t = 0; t < 4; ++t) dcol[(r + t) * 32] = v[t] == kNoSrc32 ? kTileInf : (uint32_t)v[t];
   }
-  for (; xr < n0; xr += KSEG) {
-    const int32_t v = lane < nlines ? src[(int64_t)xr * row_stride] : kNoSrc32;
-    tile[tslot(lane, xr / B, xr)] = v == kNoSrc32 ? kTileInf : (uint32_t)v;
+  for (; r < r1; ++r, src += row_stride) {
+    const int32_t v = on ? __ldg(src) : kNoSrc32;
+    dcol[r * 32] = v == kNoSrc32 ? kTileInf : (uint32_t)v;
   }
   __syncthreads();
   float *dst = out + y * n2 + zc * 32;
-  segmented_fh<float>(tile, segs, n0, nlines, dst, row_stride);
+  segmented_fh<float, WIDE>(tile, segs, n0, nlines, dst, row_stride);
 }
 
 template <typename TIn, typename TOut>
@@ -832,17 +839,17 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], dou
     // Pass Z+Y fused from the occupancy words, then pass X.
     const size_t smem_zy = (size_t)n[1] * 32 * 4 + sizeof(SegLine) * 32;
     const size_t smem_x = (size_t)n[0] * 32 * 4 + sizeof(SegLine) * 32;
-    if (smem_zy > 48 * 1024)
-      VPB_CUDA(cudaFuncSetAttribute(edt_zy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
-    if (smem_x > 48 * 1024)
-      VPB_CUDA(cudaFuncSetAttribute(edt_x_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
+    const bool wide = maxd > 512;
+    auto kzy = wide ? edt_zy_kernel<true> : edt_zy_kernel<false>;
+    auto kx = wide ? edt_x_kernel<true> : edt_x_kernel<false>;
+    if (smem_zy > 48 * 1024) VPB_CUDA(cudaFuncSetAttribute(kzy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
+    if (smem_x > 48 * 1024) VPB_CUDA(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
     const unsigned zch = (unsigned)((n[2] + 31) / 32);
-    edt_zy_kernel<<<dim3(zch, (unsigned)n[0]), ETHREADS, smem_zy, s>>>(
-        grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], (int)lo[2], (int)n[1], (int)n[2],
-        g2);
+    kzy<<<dim3(zch, (unsigned)n[0]), ETHREADS, smem_zy, s>>>(grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32),
+                                                             lo[0], lo[1], (int)lo[2], (int)n[1], (int)n[2], g2);
     rc = check_launch("edt_zy_kernel");
     if (rc) return rc;
-    edt_x_kernel<<<dim3(zch, (unsigned)n[1]), ETHREADS, smem_x, s>>>(g2, (int)n[0], (int)n[1], (int)n[2], out_sq);
+    kx<<<dim3(zch, (unsigned)n[1]), ETHREADS, smem_x, s>>>(g2, (int)n[0], (int)n[1], (int)n[2], out_sq);
     return check_launch("edt_x_kernel");
   }
   if (use_bits) {

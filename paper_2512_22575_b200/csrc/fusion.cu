@@ -36,6 +36,8 @@ struct FusionArgs {
   // fp32 prefilter constants
   float of0, of1, of2, oabs, azmax, voxf, rf[9], tf[3], tabs, fxf, fyf, cxh, cyh, ku, kv, au, av, wf, hf;
   int usable;  // pixel_masked carries bit1 = usable return (vpb_update_occupancy)
+  const int *bbox;  // optional bounding rectangle of usable pixels (chunk early-out)
+  float tauf;
   float bb_lo[3], bb_hi[3];
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr2[VPB_MAX_MASK_SPHERES];
@@ -123,10 +125,52 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
   const bool line_mask = A.n_mask > 0 && pxf >= A.bb_lo[0] && pxf <= A.bb_hi[0] && pyf >= A.bb_lo[1] &&
                          pyf <= A.bb_hi[1];
   const int64_t gline = (x * A.gy + y) * A.gz;
+  int bb_u0 = 0, bb_u1 = -1, bb_v0 = 0, bb_v1 = -1;
+  if (A.bbox) {
+    bb_u0 = __ldg(A.bbox + 0);
+    bb_u1 = __ldg(A.bbox + 1);
+    bb_v0 = __ldg(A.bbox + 2);
+    bb_v1 = __ldg(A.bbox + 3);
+  }
   for (int64_t wz = A.wz_begin; wz < A.wz_begin + A.wz_count; ++wz) {
     const int64_t z = wz * 32 + lane;
     const bool in_box = (z >= A.lo2) && (z < A.lo2 + A.n2);
+    // ---- chunk early-out (warp-uniform): the 32 voxel centres lie on a
+    // segment whose image is the segment between its endpoints' projections
+    // (qz > 0 at both ends => along it).  If that pixel range, widened by the
+    // error bound, misses every usable pixel, every voxel of the chunk is a
+    // reference "skip" -- unless the chunk may touch a mask sphere.
+    if (A.bbox) {
+      const int64_t za = wz * 32 > A.lo2 ? wz * 32 : A.lo2;
+      const int64_t zb = (wz * 32 + 31) < (A.lo2 + A.n2 - 1) ? (wz * 32 + 31) : (A.lo2 + A.n2 - 1);
+      const float pza = A.of2 + ((float)za + 0.5f) * A.voxf, pzb = A.of2 + ((float)zb + 0.5f) * A.voxf;
+      const bool maybe_mask = line_mask && !(pzb < A.bb_lo[2] || pza > A.bb_hi[2]);
+      const float qza = fmaf(A.rf[8], pza, qz0), qzb = fmaf(A.rf[8], pzb, qz0);
+      bool skip = false;
+      if (!maybe_mask) {
+        if (qza < -dq && qzb < -dq) {
+          skip = true;  // whole chunk behind the camera
+        } else if (qza > 2.0f * dq && qzb > 2.0f * dq) {
+          const float ia = __fdividef(1.0f, qza), ib = __fdividef(1.0f, qzb);
+          const float qxa = fmaf(A.rf[2], pza, qx0), qxb = fmaf(A.rf[2], pzb, qx0);
+          const float qya = fmaf(A.rf[5], pza, qy0), qyb = fmaf(A.rf[5], pzb, qy0);
+          const float ua = fmaf(A.fxf * qxa, ia, A.cxh), ub = fmaf(A.fxf * qxb, ib, A.cxh);
+          const float va = fmaf(A.fyf * qya, ia, A.cyh), vb = fmaf(A.fyf * qyb, ib, A.cyh);
+          const float ima = fmaxf(ia, ib);
+          const float du = A.ku * dq * (fmaxf(fabsf(qxa), fabsf(qxb)) + fmaxf(qza, qzb) + dq) * ima * ima +
+                           1e-6f * fmaxf(fabsf(ua), fabsf(ub)) + A.au;
+          const float dv = A.kv * dq * (fmaxf(fabsf(qya), fabsf(qyb)) + fmaxf(qza, qzb) + dq) * ima * ima +
+                           1e-6f * fmaxf(fabsf(va), fabsf(vb)) + A.av;
+          const float u_lo = fminf(ua, ub) - du - 1.0f, u_hi = fmaxf(ua, ub) + du + 1.0f;
+          const float v_lo = fminf(va, vb) - dv - 1.0f, v_hi = fmaxf(va, vb) + dv + 1.0f;
+          skip = bb_u1 < bb_u0 || u_hi < (float)bb_u0 || u_lo > (float)(bb_u1 + 1) || v_hi < (float)bb_v0 ||
+                 v_lo > (float)(bb_v1 + 1);
+        }
+      }
+      if (skip) continue;
+    }
     bool exact = false;
+    int fast = 0;  // 1 = certain hit, 2 = certain miss (fp32 classification)
     if (in_box) {
       const float pzf = A.of2 + ((float)z + 0.5f) * A.voxf;
       if (line_mask && pzf >= A.bb_lo[2] && pzf <= A.bb_hi[2]) {
@@ -156,9 +200,24 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
               exact = true;  // pixel index not certain
             } else {
               const int pix = (int)fv * (int)A.width + (int)fu;
-              exact = A.usable ? (__ldg(A.pixel_masked + pix) == 2)
-                               : (__ldg(A.pixel_masked + pix) & 1) == 0 &&
-                                     __ldg(A.depth + pix) >= A.d_min && __ldg(A.depth + pix) <= A.d_max;
+              bool usable;
+              if (A.usable) {
+                usable = __ldg(A.pixel_masked + pix) == 2;
+              } else {
+                const double m = __ldg(A.depth + pix);
+                usable = (__ldg(A.pixel_masked + pix) & 1) == 0 && m >= A.d_min && m <= A.d_max;
+              }
+              if (usable) {
+                // classification |qz - D| <= tau (hit) / qz < D - tau (miss) /
+                // occluded, decided in fp32 when clear of both boundaries
+                const float mf = (float)__ldg(A.depth + pix);
+                const float dd = qzf - mf;
+                const float e = dq + 2e-7f * (fabsf(mf) + A.tauf) + 1e-6f;
+                if (fabsf(dd) <= A.tauf - e) fast = 1;
+                else if (dd < -A.tauf - e) fast = 2;
+                else if (!(dd > A.tauf + e)) exact = true;  // near a class boundary
+                // else: certainly occluded -> skip
+              }
             }
           }
           // else: certainly outside the image -> skip
@@ -167,7 +226,19 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
     }
     bool touched = false;
     double newval = 0.0;
-    if (exact) touched = exact_voxel(A, x, y, z, gline + z, &newval);
+    if (fast) {
+      // certain hit / miss: the reference's fp64 update, bit for bit
+      const int64_t g = gline + z;
+      double value = dadd(A.log_odds[g], fast == 1 ? A.l_hit : A.l_miss);
+      if (value < A.l_min) value = A.l_min;
+      else if (value > A.l_max) value = A.l_max;
+      A.log_odds[g] = value;
+      A.observed[g] = 1;
+      newval = value;
+      touched = true;
+    } else if (exact) {
+      touched = exact_voxel(A, x, y, z, gline + z, &newval);
+    }
     if (A.occ_bits != nullptr) {
       const unsigned touched_mask = __ballot_sync(kFull, touched);
       if (touched_mask != 0u) {
@@ -189,6 +260,7 @@ struct MaskPixArgs {
   double r[9], t[3];
   int n_mask;
   int encode_usable;  // out = 1 masked, 2 usable return, 0 otherwise
+  int *bbox;          // optional: [umin, umax, vmin, vmax] of usable pixels (atomics)
   double pad;
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr[VPB_MAX_MASK_SPHERES];
@@ -218,7 +290,14 @@ __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constan
       if (dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)) < dmul(r, r)) inside = 1;
     }
   }
-  A.out[idx] = A.encode_usable ? (inside ? 1 : (valid ? 2 : 0)) : inside;
+  const uint8_t code = inside ? 1 : (valid ? 2 : 0);
+  A.out[idx] = A.encode_usable ? code : inside;
+  if (A.bbox && code == 2) {
+    atomicMin(A.bbox + 0, (int)uu);
+    atomicMax(A.bbox + 1, (int)uu);
+    atomicMin(A.bbox + 2, (int)vv);
+    atomicMax(A.bbox + 3, (int)vv);
+  }
 }
 
 // occupancy bits from log_odds: one warp per 32-voxel word.
@@ -276,7 +355,7 @@ int vpb_occ_bits_from_log_odds(const vpb_grid *grid, double thr, void *stream) {
 
 static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const double *centers,
                               const double *radii, int64_t n_mask, double pad, uint8_t *out, int encode,
-                              void *stream) {
+                              int *bbox, void *stream) {
   VPB_REQUIRE(depth && cam && out, "null argument to vpb_masked_pixels");
   MaskPixArgs A;
   memset(&A, 0, sizeof(A));
@@ -294,6 +373,7 @@ static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const 
   memcpy(A.t, cam->pose_t, sizeof(A.t));
   A.n_mask = (int)n_mask;
   A.encode_usable = encode;
+  A.bbox = bbox;
   A.pad = pad;
   const int64_t npx = cam->width * cam->height;
   if (npx == 0) return VPB_OK;
@@ -303,7 +383,8 @@ static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const 
 
 static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
                      const double *depth, const uint8_t *pixel_masked, const double *centers,
-                     const double *radii, int64_t n_mask, const vpb_map_params *p, int usable, void *stream) {
+                     const double *radii, int64_t n_mask, const vpb_map_params *p, int usable, const int *bbox,
+                     void *stream) {
   VPB_REQUIRE(grid && grid->log_odds && grid->observed && cam && depth && pixel_masked && p,
               "null argument to vpb_fuse_voxels");
   for (int k = 0; k < 3; ++k)
@@ -336,6 +417,8 @@ static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
   A.l_min = p->l_min; A.l_max = p->l_max; A.l_thr = p->l_occ_threshold;
   A.n_mask = (int)n_mask;
   A.usable = usable;
+  A.bbox = bbox;
+  A.tauf = (float)A.tau;
   A.of0 = (float)A.origin0;
   A.of1 = (float)A.origin1;
   A.of2 = (float)A.origin2;
@@ -372,23 +455,29 @@ static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
 
 int vpb_masked_pixels(const double *depth, const vpb_camera *cam, const double *centers, const double *radii,
                       int64_t n_mask, double pad, uint8_t *out, void *stream) {
-  return masked_pixels_impl(depth, cam, centers, radii, n_mask, pad, out, 0, stream);
+  return masked_pixels_impl(depth, cam, centers, radii, n_mask, pad, out, 0, nullptr, stream);
 }
 
 int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
                     const double *depth, const uint8_t *pixel_masked, const double *centers, const double *radii,
                     int64_t n_mask, const vpb_map_params *p, void *stream) {
-  return fuse_impl(grid, lo, n, cam, depth, pixel_masked, centers, radii, n_mask, p, 0, stream);
+  return fuse_impl(grid, lo, n, cam, depth, pixel_masked, centers, radii, n_mask, p, 0, nullptr, stream);
 }
 
 int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
                          const double *depth, const double *centers, const double *radii, int64_t n_mask,
                          double mask_pad, const vpb_map_params *params, uint8_t *pixel_scratch, void *stream) {
   VPB_REQUIRE(pixel_scratch, "pixel scratch is null");
-  // pixel classes in one byte: 1 = return on the robot body, 2 = usable return
-  int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, stream);
+  // pixel classes in one byte: 1 = return on the robot body, 2 = usable
+  // return; followed by the bounding rectangle of the usable pixels
+  const int64_t npx = cam->width * cam->height;
+  int *bbox = reinterpret_cast<int *>(pixel_scratch + align_up((size_t)npx, 16));
+  VPB_CUDA(cudaMemsetAsync(bbox, 0x7F, 16, as_stream(stream)));
+  VPB_CUDA(cudaMemsetAsync(bbox + 1, 0x80, 4, as_stream(stream)));
+  VPB_CUDA(cudaMemsetAsync(bbox + 3, 0x80, 4, as_stream(stream)));
+  int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, bbox, stream);
   if (rc) return rc;
-  return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, stream);
+  return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, bbox, stream);
 }
 
 }  // extern "C"
