@@ -297,3 +297,30 @@ def smpc_step(args: dict, nominal, eps, lam: float, acc_limits):
     return {"u": u, "command": command, "next_nominal": next_nominal, "costs": res["costs"],
             "weighted_cost": float(weighted["costs"][0]), "weighted_terms": weighted["terms"][0],
             "best_cost": float(res["costs"].min())}
+
+
+# ---------------------------------------------------------------------------
+# sharded softmin protocol (SURVEY.md section 8e) -- checker for the N-rank
+# exchange: per-rank partial, then the fixed rank-order log-sum-exp merge.
+# ---------------------------------------------------------------------------
+def smpc_partial(costs, eps, lam: float, m_offset: int = 0) -> np.ndarray:
+    """[m_r, Z_r, nonfinite_r, best_index_r, N_r (H n)] of one shard."""
+    costs = _c(costs)
+    eps = np.asarray(eps, dtype=np.float64)
+    fin = np.isfinite(costs)
+    m = costs[fin].min() if fin.any() else np.inf
+    w = np.where(fin, np.exp(-(costs - m) / lam), 0.0) if np.isfinite(m) else np.zeros_like(costs)
+    best = float(m_offset + int(np.argmin(np.where(fin, costs, np.inf)))) if fin.any() else -1.0
+    n_r = np.einsum("m,mk->k", w, eps.reshape(eps.shape[0], -1))
+    return np.concatenate([[m, w.sum(), float((~fin).sum()), best], n_r])
+
+
+def merge_partials(parts, lam: float):
+    """Merge rank partials in rank order -> (min, Z, nonfinite, best, N/Z)."""
+    parts = np.asarray(parts, dtype=np.float64)
+    m = parts[:, 0].min()
+    scale = np.exp(-(parts[:, 0] - m) / lam)
+    z = float((parts[:, 1] * scale).sum())
+    n = (parts[:, 4:] * scale[:, None]).sum(axis=0)
+    r_best = int(np.argmin(parts[:, 0]))
+    return m, z, float(parts[:, 2].sum()), parts[r_best, 3], n / z

@@ -48,16 +48,21 @@ class ShardedSMPC:
     def global_samples(self) -> int:
         return self.world * self.m_local
 
+    def sample_range(self) -> tuple[int, int]:
+        """Global sample indices [lo, hi) this rank evaluates (rank 0 holds the nominal, sample 0)."""
+        lo = self.rank * self.m_local
+        return lo, lo + self.m_local
+
     def step_device(self, state, goal, snap, nominal_dev: torch.Tensor, rng_seed: int,
                     perturbations: torch.Tensor | None = None) -> torch.Tensor:
         pl = self.planner
         if perturbations is None:
-            eps = pl.sample_device(rng_seed, m_offset=self.rank * self.m_local, samples=self.m_local)
+            eps = pl.sample_device(rng_seed, m_offset=self.sample_range()[0], samples=self.m_local)
         else:
             eps = perturbations
         if self.world == 1:
             return pl.smpc_step_device(state, goal, snap, nominal_dev, eps)  # one fused launch
-        part, _, _ = pl.smpc_partial_device(state, goal, snap, nominal_dev, eps, m_offset=self.rank * self.m_local)
+        part, _, _ = pl.smpc_partial_device(state, goal, snap, nominal_dev, eps, m_offset=self.sample_range()[0])
         parts = exchange_partials(part, self.world, self.group)
         return pl.smpc_finish_device(state, goal, snap, nominal_dev, parts)
 

@@ -3,6 +3,7 @@ and exports every entry point include/vpb200.h declares (no compute calls)."""
 
 import ctypes
 import re
+import sys
 from pathlib import Path
 
 import pytest
@@ -96,3 +97,38 @@ def test_product_never_imports_oracle():
     for path in (ROOT / "paper_2512_22575_b200").rglob("*.py"):
         text = path.read_text()
         assert "import oracle" not in text and "from oracle" not in text, path
+
+
+def test_reference_shim_packs_like_planner():
+    """integration/voxplan_shim.py packs evaluate_batch's flat arguments
+    (vp/batch.py:162-195) into the same vpb_problem block as Planner."""
+    import ctypes
+
+    import numpy as np
+
+    sys_path_root = str(ROOT / "integration")
+    if sys_path_root not in sys.path:
+        sys.path.insert(0, sys_path_root)
+    import voxplan_shim
+    from paper_2512_22575_b200 import config, planner
+
+    chain, model = config.robot_7dof()
+    params = config.planner_params(7, {"samples": 16, "horizon": 12})
+    want = planner.pack_problem(chain, model, params)
+    lims = planner.tightened_limits(chain, params.margin_frac)
+    got = voxplan_shim.problem_from_reference_args(
+        np.zeros(7), np.zeros(7), params.dt, chain.base_pose.rotation.matrix, chain.base_pose.translation,
+        np.array([j.parent_offset.rotation.matrix for j in chain.joints]),
+        np.array([j.parent_offset.translation for j in chain.joints]), np.array([j.axis for j in chain.joints]),
+        np.array([s.link for s in model.spheres]), np.array([s.center for s in model.spheres]), model.radii(),
+        np.array(model.self_pairs), np.eye(3), np.zeros(3), params.pose_weight, params.terminal_weight, *lims,
+        params.w_env, params.w_self, params.w_q, params.w_qd, params.w_qdd, params.w_s, params.w_ns, params.d_act,
+        params.q_ref, params.horizon)
+    for name, _ in want._fields_:
+        if name in ("acc_limit", "lam", "goal_r", "goal_t", "q0", "qd0", "dyn_state"):
+            continue  # per-call / step-only fields the evaluate seam does not carry
+        a, b = getattr(want, name), getattr(got, name)
+        if isinstance(a, ctypes.Array):
+            assert list(a) == list(b), name
+        else:
+            assert a == b, name
