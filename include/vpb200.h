@@ -258,6 +258,15 @@ int vpb_sample_perturbations(uint64_t seed, const uint64_t *seed_dev,
                              int64_t window, const double *sigma, int dtype,
                              void *out, void *stream);
 
+/* ------------------------------------------------------------------------ */
+/* Diagnostics                                                               */
+/* ------------------------------------------------------------------------ */
+/* Phase timestamps (%globaltimer, ns) of subsequent SMPC launches into a
+ * device buffer of >= 2 * ceil(M / 4) + 16 uint64: per CTA [start, candidates
+ * done], then [group merges done, global merge done, step done].  NULL turns
+ * it off (tools/smpc_trace.py). */
+void vpb_debug_smpc_trace(unsigned long long *dev_buffer);
+
 #ifdef __cplusplus
 }
 #endif

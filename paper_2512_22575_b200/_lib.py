@@ -111,6 +111,7 @@ SIGNATURES = {
                                        _sz, _p]),
     "vpb_sample_perturbations": (ctypes.c_int, [ctypes.c_uint64, _p, _i64, _i64, _i64, _i64, _i64, _p,
                                                 ctypes.c_int, _p, _p]),
+    "vpb_debug_smpc_trace": (None, [_p]),
 }
 
 _lib: ctypes.CDLL | None = None

@@ -25,12 +25,14 @@
 // partial is what ranks all-gather; vpb_smpc_finish merges the
 // rank partials in rank order and runs the same tail.
 #include <cfloat>
+#include <cstdlib>
 
-#include "rollout.cuh"
+#include "rollout_fixed.cuh"
 
 namespace vpb {
 
-constexpr int NW = 8;                    // candidate warps per CTA
+constexpr int NW = 8;                    // candidate warps per CTA (generic path, rollout kernel)
+constexpr int NWF = 4;                   // candidate warps per CTA of the fixed-topology SMPC kernel
 constexpr int kThreads = (NW + 1) * 32;  // + terminal warp
 constexpr int kPartHead = 4;             // [m, Z, nonfinite, best_index]
 constexpr int kGroup = 32;               // CTAs merged by a group's last CTA
@@ -58,6 +60,25 @@ __device__ __forceinline__ double warp_sum_d(double x) {
   return x;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// trace layout: [cta * 2 + 0] = start, [cta * 2 + 1] = candidates done,
+// then at 2 * ctas: [group merge done, global merge done, tail done]
+#define VPB_TRACE(io, idx)                                      \
+  do {                                                          \
+    if ((io).trace && threadIdx.x == 0) (io).trace[idx] = gtimer(); \
+  } while (0)
+
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ double dinf() { return __longlong_as_double(0x7ff0000000000000ll); }
 
 template <typename ET>
@@ -69,7 +90,7 @@ __device__ __forceinline__ double load_e(const ET *p) {
 // shared memory layout (same computation on host and device)
 // ---------------------------------------------------------------------------
 struct SmemLayout {
-  size_t centers, sums, cost, qH, fail, tfail, dyn, misc, scratch, total;
+  size_t centers, sums, cost, qH, fail, tfail, dyn, pro, misc, scratch, total;
 };
 
 __host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
@@ -91,10 +112,12 @@ __host__ __device__ inline SmemLayout smem_layout(int ns, size_t tsize, int scra
   o = al16(o + (size_t)NW * 4);
   L.dyn = o;
   o = al16(o + (size_t)(2 * kMaxJ + 12) * tsize);
+  L.pro = o;  // q_0 terms of the fixed-topology path (see pro_fail)
+  o = al16(o + 8 * 8);
   L.misc = o;  // 32 doubles of reduction scratch + flags
   o = al16(o + 48 * 8);
-  L.scratch = o;  // merge scales
-  o = al16(o + (size_t)(scratch_doubles > 0 ? scratch_doubles : 1) * 8);
+  L.scratch = o;  // merge scales + compacted row indices (and the finish kernel's split sums)
+  o = al16(o + (size_t)(2 * (scratch_doubles > 32 ? scratch_doubles : 32) + 24) * 8);
   L.total = o;
   return L;
 }
@@ -319,6 +342,7 @@ struct Shared {
   void *qH;
   int *fail, *tfail;
   void *dyn;
+  double *pro;
   double *misc, *scratch;
 };
 
@@ -331,6 +355,7 @@ __device__ __forceinline__ Shared carve(unsigned char *base, const SmemLayout &L
   S.fail = reinterpret_cast<int *>(base + L.fail);
   S.tfail = reinterpret_cast<int *>(base + L.tfail);
   S.dyn = base + L.dyn;
+  S.pro = reinterpret_cast<double *>(base + L.pro);
   S.misc = reinterpret_cast<double *>(base + L.misc);
   S.scratch = reinterpret_cast<double *>(base + L.scratch);
   return S;
@@ -365,6 +390,164 @@ __device__ __forceinline__ void evaluate_cta(const Prob<T> &P, const Dyn<T> &D, 
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// Fixed-topology candidate (rollout_fixed.cuh): lane k integrates to q_{k+1}
+// and evaluates FK there; the limit terms use (q_k, qd_k, u_k).  Leaves the
+// running sums (without the q_0 terms), the terminal cost and the flag.
+// ---------------------------------------------------------------------------
+struct TopoDyn {};  // marker: runtime topology (generic path)
+
+template <typename Topo>
+constexpr bool is_dyn_v = std::is_same_v<Topo, TopoDyn>;
+
+// smpc_kernel shape: the generic path has a terminal warp per CTA; the fixed
+// path has candidate warps only (its q_0 terms are added by the last CTA).
+template <typename Topo>
+constexpr int smpc_nw() {
+  return is_dyn_v<Topo> ? NW : NWF;
+}
+template <typename Topo>
+constexpr int smpc_threads() {
+  return is_dyn_v<Topo> ? (NW + 1) * 32 : NWF * 32;
+}
+// fp32 fixed path: 7 CTAs of 4 warps per SM (<= 72 registers) so that a
+// 4096-candidate step runs in a single wave on 148 SMs.
+template <typename T, typename Topo>
+constexpr int smpc_min_blocks() {
+  return sizeof(T) == 8 ? 1 : (is_dyn_v<Topo> ? 2 : 7);
+}
+
+// One fixed-topology evaluation per warp, lane = step.  The warp integrates
+// u_k = ctrl[k] + nominal[k] (either may be null = 0) from (q0, qd0) and
+// evaluates the configuration q_{k+shift}: shift 1 is a candidate (running
+// pose + spheres for k+1 < H, terminal pose for k+1 == H); shift 0 with H = 1
+// is the q_0 prologue (lane 0: pose + spheres at q_0; its limit terms are
+// ignored).  Every caller goes through one call site per kernel so the
+// unrolled step code exists once in the instruction stream.
+template <typename T, typename ET, typename Topo>
+__device__ __forceinline__ void fixed_candidate(const Prob<T> &P, const Dyn<T> &D, const ET *ctrl,
+                                                const double *nominal, bool valid, int H, int shift, int sub,
+                                                int nsub, double *sums_slot, double *term_slot, int *fail_slot) {
+  constexpr int NJ = Topo::NJ;
+  const int lane = threadIdx.x & 31;
+  const Split W = make_split<Topo>(sub, nsub);
+  const bool do_lim = sub == 0;
+  T qc[NJ], qdc[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    qc[j] = D.q0[j];
+    qdc[j] = D.qd0[j];
+  }
+  T s_pose = 0, s_coll = 0, s_lim = 0, s_smooth = 0, s_null = 0, term = 0;
+  bool fail = false;
+  const int nchunks = (H + 31) >> 5;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int k = ch * 32 + lane;
+    const bool act = valid && k < H;
+    T qe[NJ];
+    T lim = 0, sm = 0, nu = 0;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      double v = 0.0;
+      if (act) {
+        if (ctrl) v = load_e<ET>(ctrl + (size_t)k * NJ + j);
+        if (nominal) v += nominal[(size_t)k * NJ + j];
+      }
+      const T uj = (T)v;
+      const T vdt = uj * P.dt;
+      const T vin = warp_incl_scan<T>(vdt, lane);
+      const T qd = qdc[j] + (vin - vdt);          // qd_k
+      const T qdn = act ? (qdc[j] + vin) : T(0);  // qd_{k+1}
+      const T w = qdn * P.dt;
+      const T win = warp_incl_scan<T>(w, lane);
+      const T q = qc[j] + (win - w);              // q_k
+      qe[j] = shift ? qc[j] + win : q;            // q_{k+shift}
+      qdc[j] += __shfl_sync(kFull, vin, 31);
+      qc[j] += __shfl_sync(kFull, win, 31);
+      // limits / smoothness / null space at step k (vp/batch.py:303-311)
+      const T vq = bound_violation<T>(q, P.pos_lo[j], P.pos_hi[j]);
+      const T vv = bound_violation<T>(qd, P.vel_lo[j], P.vel_hi[j]);
+      const T va = bound_violation<T>(uj, P.acc_lo[j], P.acc_hi[j]);
+      lim += P.w_q * vq * vq + P.w_qd * vv * vv + P.w_qdd * va * va;
+      sm += P.w_s * uj * uj;
+      const T dq = q - P.q_ref[j];
+      nu += P.w_ns * dq * dq;
+    }
+    if (act) {
+      if (do_lim) {
+        s_lim += lim;
+        s_smooth += sm;
+        s_null += nu;
+      }
+      const int idx = k + shift;
+      const bool last = idx == H;
+      T pose, coll;
+      if (!fixed_config<Topo, T>(P, P.fc, D, qe, !last, last, W, pose, coll)) fail = true;
+      if (last) term = pose;
+      else s_pose += pose;
+      s_coll += coll;
+    }
+  }
+  const double r_pose = warp_sum_d((double)s_pose);
+  const double r_coll = warp_sum_d((double)s_coll);
+  const double r_lim = warp_sum_d((double)s_lim);
+  const double r_smooth = warp_sum_d((double)s_smooth);
+  const double r_null = warp_sum_d((double)s_null);
+  const double r_term = warp_sum_d((double)term);  // one lane holds it
+  const bool any_fail = __any_sync(kFull, fail);
+  if (lane == 0) {
+    sums_slot[0] = r_pose;
+    sums_slot[1] = r_coll;
+    sums_slot[2] = r_lim;
+    sums_slot[3] = r_smooth;
+    sums_slot[4] = r_null;
+    *term_slot = r_term;
+    *fail_slot = any_fail ? 1 : 0;
+  }
+}
+
+// S.pro layout: [0..5] prologue sums (pose, collision, ...), [6] terminal
+// (unused), int at [7] = failed.
+__device__ __forceinline__ int *pro_fail(const Shared &S) { return reinterpret_cast<int *>(S.pro + 7); }
+
+// Add the q_0 terms to candidate w's sums (after a __syncthreads).
+__device__ __forceinline__ void fixed_add_prologue(const Shared &S, int w) {
+  S.sums[w * 6 + 0] += S.pro[0];
+  S.sums[w * 6 + 1] += S.pro[1];
+  if (*pro_fail(S) != 0) S.fail[w] = 1;
+  S.tfail[w] = 0;
+}
+
+// rollout_kernel, fixed path: warps < NW are candidates, warp NW the q_0
+// prologue, through one call site.
+template <typename T, typename ET, typename Topo>
+__device__ __forceinline__ void evaluate_cta_fixed(const Prob<T> &P, const Dyn<T> &D, const ET *ctrl,
+                                                   const double *nominal, int64_t M, int64_t cta_m0,
+                                                   const Shared &S) {
+  const int warp = threadIdx.x >> 5;
+  const bool cand = warp < NW;
+  const int64_t m = cta_m0 + warp;
+  const bool valid = cand ? m < M : true;
+  fixed_candidate<T, ET, Topo>(P, D, (cand && valid) ? ctrl + (size_t)m * P.H * Topo::NJ : nullptr,
+                               cand ? nominal : nullptr, valid, cand ? P.H : 1, cand ? 1 : 0, 0, 1,
+                               cand ? S.sums + warp * 6 : S.pro, cand ? S.cost + warp : S.pro + 6,
+                               cand ? S.fail + warp : pro_fail(S));
+  __syncthreads();
+  if (threadIdx.x < NW) fixed_add_prologue(S, threadIdx.x);
+  __syncthreads();
+}
+
+template <typename T, typename ET, int MAXJ, typename Topo>
+__device__ __forceinline__ void evaluate_cta_any(const Prob<T> &P, const Dyn<T> &D, const ET *ctrl,
+                                                 const double *nominal, int64_t M, int64_t cta_m0, const Shared &S,
+                                                 const CandOut &co) {
+  if constexpr (std::is_same_v<Topo, TopoDyn>) {
+    evaluate_cta<T, ET, MAXJ>(P, D, ctrl, nominal, M, cta_m0, S, co);
+  } else {
+    evaluate_cta_fixed<T, ET, Topo>(P, D, ctrl, nominal, M, cta_m0, S);
+  }
+}
+
 struct RolloutIO {
   const void *ctrl;       // M x H x n (ET)
   const double *nominal;  // H x n or null
@@ -377,18 +560,18 @@ struct RolloutIO {
 };
 
 // evaluate_batch (vp/batch.py:161-336)
-template <typename T, typename ET, int MAXJ>
+template <typename T, typename ET, int MAXJ, typename Topo>
 __global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) rollout_kernel(const __grid_constant__ Prob<T> P,
                                                               const __grid_constant__ RolloutIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const SmemLayout L = smem_layout(P.ns, sizeof(T), 0);
+  const SmemLayout L = smem_layout(std::is_same_v<Topo, TopoDyn> ? P.ns : 0, sizeof(T), 0);
   const Shared S = carve(smem_raw, L);
   Dyn<T> &D = *reinterpret_cast<Dyn<T> *>(S.dyn);
   if (threadIdx.x < 32) load_dyn<T>(P, io.dyn, D);
   __syncthreads();
   const int64_t cta_m0 = (int64_t)blockIdx.x * NW;
   CandOut co{io.traj_q, io.traj_qd, io.sph_out};
-  evaluate_cta<T, ET, MAXJ>(P, D, reinterpret_cast<const ET *>(io.ctrl), io.nominal, io.M, cta_m0, S, co);
+  evaluate_cta_any<T, ET, MAXJ, Topo>(P, D, reinterpret_cast<const ET *>(io.ctrl), io.nominal, io.M, cta_m0, S, co);
   if (threadIdx.x < NW) {
     const int w = threadIdx.x;
     const int64_t m = cta_m0 + w;
@@ -423,22 +606,49 @@ __device__ __forceinline__ double block_sum_fixed(double v, double *misc) {
   return t;
 }
 
-__device__ void merge_block(const double *src, int count, int hn, double lam, double *dst, double *scale,
-                            double *misc) {
-  const int L = kPartHead + hn;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  // min (exact, order-free) with the smallest index among equal minima
+// Partial rows to merge: head field f of row i at head[f * fstride + i *
+// rstride] (fields m, Z, non-finite, best); N of row i at n[i * nstride].
+// CTA partials are structure-of-arrays (fstride = rows, rstride = 1: a warp
+// reads 32 consecutive heads with one coalesced load); rank records are the
+// exchanged [m, Z, nf, best, N] rows (fstride = 1, rstride = nstride = L).
+struct Rows {
+  const double *head;
+  const double *n;
+  int64_t fstride, rstride, nstride;
+  __device__ __forceinline__ double h(int f, int i) const { return head[f * fstride + (int64_t)i * rstride]; }
+};
+
+__device__ void merge_block(const Rows &R, int count, int hn, double lam, double *dst, double *scratch,
+                            double *misc, unsigned long long *trace_head = nullptr) {
+  // Merge `count` partial rows in row order.  Warp w owns the contiguous rows
+  // [w span, (w + 1) span), lanes over consecutive rows (coalesced):
+  //   1. min and the first row attaining it;
+  //   2. scale_i = exp(-(m_i - min) / lam), Z = sum scale_i Z_i, non-finite
+  //      count (lane-strided partial sums, then a fixed xor tree and the
+  //      warps in order -- deterministic);
+  //   3. rows with scale 0 (exp underflow: far above the minimum -- most of
+  //      them at the planner's lam) are dropped by an order-preserving
+  //      ballot compaction, and N = sum scale_i N_i runs over the rest.
+  // scratch: >= 2 * (count + 512) + 24 doubles; misc: >= 48 doubles.
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const int span = ((count + nw - 1) / nw + 31) & ~31;
+  const int w0 = warp * span, w1 = min(count, w0 + span);
   double mn = dinf();
-  double bi = -1.0;
   int bidx = 0x7fffffff;
-  for (int i = tid; i < count; i += nt) {
-    const double v = src[(size_t)i * L];
-    if (v < mn || (v == mn && i < bidx)) {
-      mn = v;
-      bidx = i;
+  for (int c = w0; c < w1; c += 32 * 4) {
+    double v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int i = c + 32 * t + lane;
+      v[t] = i < w1 ? R.h(0, i) : dinf();
     }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (v[t] < mn) {  // rows ascend per lane: the first minimum wins
+        mn = v[t];
+        bidx = c + 32 * t + lane;
+      }
   }
-  // warp argmin
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) {
     const double ov = __shfl_xor_sync(kFull, mn, d);
@@ -448,16 +658,16 @@ __device__ void merge_block(const double *src, int count, int hn, double lam, do
       bidx = oi;
     }
   }
-  __syncthreads();
-  if ((tid & 31) == 0) {
-    misc[tid >> 5] = mn;
-    misc[16 + (tid >> 5)] = (double)bidx;
+  if (lane == 0) {
+    misc[warp] = mn;
+    misc[16 + warp] = (double)bidx;
   }
+  if (trace_head && tid == 0) trace_head[1] = gtimer();
   __syncthreads();
   if (tid == 0) {
     double m0 = dinf();
     int b0 = 0x7fffffff;
-    for (int w = 0; w < (nt >> 5); ++w) {
+    for (int w = 0; w < nw; ++w) {
       const double v = misc[w];
       const int b = (int)misc[16 + w];
       if (v < m0 || (v == m0 && b < b0)) {
@@ -466,47 +676,90 @@ __device__ void merge_block(const double *src, int count, int hn, double lam, do
       }
     }
     misc[40] = m0;
-    misc[41] = (b0 >= 0 && b0 < count) ? src[(size_t)b0 * L + 3] : -1.0;
+    misc[41] = (double)b0;
   }
   __syncthreads();
   mn = misc[40];
-  bi = misc[41];
-  for (int i = tid; i < count; i += nt) {
-    const double v = src[(size_t)i * L];
-    scale[i] = (v < dinf()) ? exp(-(v - mn) / lam) : 0.0;
+  bidx = (int)misc[41];
+  // pass 2: scales, Z, non-finite count, and the order-preserving compaction
+  // of this warp's nonzero rows into its own slice [w0, w0 + wnz) of the
+  // row list (rows ascend within a warp; warps are concatenated in order)
+  const int cap = count + 32 * nw;  // per-warp slices may overhang count
+  double *scale = scratch;
+  int *rows = reinterpret_cast<int *>(scratch + cap);
+  double *nf_w = scratch + cap + cap / 2 + 2;
+  const double inv_lam = 1.0 / lam;
+  double z = 0.0, nf = 0.0;
+  int wnz = 0;
+  for (int c = w0; c < w1; c += 32 * 4) {
+    double v[4], zi[4], fi[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int i = c + 32 * t + lane;
+      const bool ok = i < w1;
+      v[t] = ok ? R.h(0, i) : dinf();
+      zi[t] = ok ? R.h(1, i) : 0.0;
+      fi[t] = ok ? R.h(2, i) : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const double sc = (v[t] < dinf()) ? exp(-(v[t] - mn) * inv_lam) : 0.0;
+      if (sc != 0.0) z += sc * zi[t];
+      nf += fi[t];
+      const unsigned bal = __ballot_sync(kFull, sc != 0.0);
+      if (sc != 0.0) {
+        const int p = w0 + wnz + __popc(bal & ((1u << lane) - 1u));
+        rows[p] = c + 32 * t + lane;
+        scale[p] = sc;
+      }
+      wnz += __popc(bal);
+    }
   }
+  const double zw = warp_sum_d(z), nfw = warp_sum_d(nf);
+  if (lane == 0) {
+    misc[16 + warp] = (double)wnz;  // (misc[16..32) is free again)
+    misc[32 + warp] = zw;
+    nf_w[warp] = nfw;
+  }
+  if (trace_head && tid == 0) trace_head[2] = gtimer();
   __syncthreads();
-  double zpart = 0.0, nfpart = 0.0;
-  for (int i = tid; i < count; i += nt) {
-    if (scale[i] != 0.0) zpart += scale[i] * src[(size_t)i * L + 1];
-    nfpart += src[(size_t)i * L + 2];
-  }
-  const double Z = block_sum_fixed(zpart, misc);
-  const double nf = block_sum_fixed(nfpart, misc);
   if (tid == 0) {
+    double Z = 0.0, NF = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      Z += misc[32 + w];
+      NF += nf_w[w];
+    }
     dst[0] = mn;
     dst[1] = Z;
-    dst[2] = nf;
-    dst[3] = bi;
+    dst[2] = NF;
+    dst[3] = (bidx >= 0 && bidx < count) ? R.h(3, bidx) : -1.0;
   }
+  if (trace_head && tid == 0) *trace_head = gtimer();
+  // N over the nonzero rows, warp slices in order
   for (int e = tid; e < hn; e += nt) {
+    const double *col = R.n + e;
     double acc = 0.0;
-    int i = 0;
-    for (; i + 4 <= count; i += 4) {
-      const double a0 = src[(size_t)i * L + kPartHead + e];
-      const double a1 = src[(size_t)(i + 1) * L + kPartHead + e];
-      const double a2 = src[(size_t)(i + 2) * L + kPartHead + e];
-      const double a3 = src[(size_t)(i + 3) * L + kPartHead + e];
-      if (scale[i] != 0.0) acc += scale[i] * a0;
-      if (scale[i + 1] != 0.0) acc += scale[i + 1] * a1;
-      if (scale[i + 2] != 0.0) acc += scale[i + 2] * a2;
-      if (scale[i + 3] != 0.0) acc += scale[i + 3] * a3;
+    for (int w = 0; w < nw; ++w) {
+      const int base = w * span, cnt = (int)misc[16 + w];
+      int k = 0;
+      for (; k + 4 <= cnt; k += 4) {
+        double a[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) a[t] = col[(int64_t)rows[base + k + t] * R.nstride];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc += scale[base + k + t] * a[t];
+      }
+      for (; k < cnt; ++k) acc += scale[base + k] * col[(int64_t)rows[base + k] * R.nstride];
     }
-    for (; i < count; ++i)
-      if (scale[i] != 0.0) acc += scale[i] * src[(size_t)i * L + kPartHead + e];
     dst[kPartHead + e] = acc;
   }
   __syncthreads();
+}
+
+// Rank records [m, Z, nf, best, N (hn)] as merge rows.
+__device__ __forceinline__ Rows record_rows(const double *rec, int hn) {
+  const int L = kPartHead + hn;
+  return Rows{rec, rec + kPartHead, 1, L, L};
 }
 
 struct AccLimit {
@@ -529,14 +782,16 @@ struct SmpcIO {
   double *out;             // step output (see vpb_smpc_out_len)
   AccLimit acc;
   const double *dyn;
+  unsigned long long *trace;  // optional per-phase %globaltimer stamps (tools/smpc_trace.py)
+  double *pro;  // [NWF][4] q_0 terms per split warp (fixed path, prologue block 0)
+  double *cand_costs;  // [M] candidate costs when io.costs is null (workspace)
 };
 
-// U*, clip, shift, then the M = 1 re-evaluation of U* (vp/planner.py:614-629)
-// on warps 0 and NW of the calling CTA.  `part` is the fully merged partial.
-template <typename T, int MAXJ>
-__device__ void smpc_tail(const Prob<T> &P, const Dyn<T> &D, const double *part, const double *nominal,
-                          const AccLimit &acc, double *out, const Shared &S) {
-  const int H = P.H, n = P.nj, hn = H * n;
+// U* = nominal + N / Z, the clipped command and the shifted warm start
+// (vp/planner.py:614-619), written to `out` by all threads of the CTA.
+__device__ __forceinline__ void tail_controls(const double *part, const double *nominal, const AccLimit &acc, int H,
+                                              int n, double *out) {
+  const int hn = H * n;
   const double Z = part[1];
   for (int e = threadIdx.x; e < hn; e += blockDim.x) {
     const double u = nominal[e] + part[kPartHead + e] / Z;
@@ -549,6 +804,30 @@ __device__ void smpc_tail(const Prob<T> &P, const Dyn<T> &D, const double *part,
     }
   }
   for (int e = threadIdx.x; e < n; e += blockDim.x) out[hn + n + hn - n + e] = 0.0;
+}
+
+// Diagnostics of the step (thread 0): re-evaluated cost of U* from slot 0 of
+// S (sums / cost / flags), best cost, Z, non-finite count, best index.
+__device__ __forceinline__ void tail_output(const Shared &S, const double *part, int H, int n, double best,
+                                            double nonfinite, double *out) {
+  if (threadIdx.x != 0) return;
+  const int64_t base = 2 * (int64_t)H * n + n;
+  const bool failed = S.fail[0] != 0 || S.tfail[0] != 0;
+  const double *sm = S.sums;
+  out[base] = failed ? dinf() : sm[0] + sm[1] + sm[2] + sm[3] + sm[4] + S.cost[0];
+  for (int a = 0; a < 5; ++a) out[base + 1 + a] = failed ? 0.0 : sm[a];
+  out[base + 6] = failed ? 0.0 : S.cost[0];
+  out[base + 7] = best;
+  out[base + 8] = part[1];    // Z
+  out[base + 9] = nonfinite;  // non-finite sample count
+  out[base + 10] = part[3];   // best sample index
+}
+
+// Generic path tail: U*, then its M = 1 re-evaluation on warps 0 and NW.
+template <typename T, int MAXJ>
+__device__ void smpc_tail_dyn(const Prob<T> &P, const Dyn<T> &D, const double *part, const double *nominal,
+                              const AccLimit &acc, double *out, const Shared &S) {
+  tail_controls(part, nominal, acc, P.H, P.nj, out);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   T *centers = reinterpret_cast<T *>(S.centers);
@@ -566,163 +845,401 @@ __device__ void smpc_tail(const Prob<T> &P, const Dyn<T> &D, const double *part,
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const int64_t base = 2 * hn + n;
-    const bool failed = S.fail[0] != 0 || S.tfail[0] != 0;
-    const double *sm = S.sums;
-    out[base] = failed ? dinf() : sm[0] + sm[1] + sm[2] + sm[3] + sm[4] + S.cost[0];
-    for (int a = 0; a < 5; ++a) out[base + 1 + a] = failed ? 0.0 : sm[a];
-    out[base + 6] = failed ? 0.0 : S.cost[0];
-    out[base + 7] = part[0];   // best cost
-    out[base + 8] = Z;
-    out[base + 9] = part[2];   // non-finite sample count
-    out[base + 10] = part[3];  // best sample index
+  tail_output(S, part, P.H, P.nj, part[0], part[2], out);
+}
+
+// Fixed path: add the q_0 terms (S.pro) to this shard's per-sample costs and,
+// when `part` is given, to its merged partial's minimum (the softmin weights
+// are shift invariant, so Z and N are unchanged).
+__device__ __forceinline__ void fixed_shard_fixup(const Shared &S, int64_t M, double *costs, uint8_t *flags,
+                                                  double *part) {
+  const bool bad = *pro_fail(S) != 0;
+  const double add = S.pro[0] + S.pro[1];
+  for (int64_t m = threadIdx.x; m < M; m += blockDim.x) {
+    if (costs) costs[m] = bad ? dinf() : costs[m] + add;
+    if (flags && bad) flags[m] = 1;
   }
+  if (threadIdx.x == 0 && part) {
+    part[0] = bad ? dinf() : part[0] + add;
+    if (bad) part[2] = (double)M;
+  }
+}
+
+// Per-candidate totals -> CTA softmin partial -> group merge by the group's
+// last CTA -> global merge by the last group into io.rank_part.  Returns
+// true on the CTA that did the global merge (all others are done).
+// Final merge of the single-device step, by the last CTA.  Inputs: the CTA
+// heads (structure-of-arrays [3][ctas]: min cost, non-finite count, best
+// global index) and every candidate's cost.  Output: the shard record
+// [min, Z, non-finite, best, N (hn)] with weights w_m = exp(-(S_m - min)/lam)
+// in candidate order.  A CTA whose own minimum is far above the global one
+// (exp underflow) contributes exactly zero and is skipped before any of its
+// candidates is touched; at the planner's lam almost all are.
+template <typename ET, int NWC>
+__device__ void final_merge(const SmpcIO &io, const Shared &S, const double *heads, const double *costs, int ctas,
+                            int hn, unsigned long long *trace_head) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  double *misc = S.misc;
+  double *wlist = io.group_parts;                                  // candidate weights (scratch)
+  int *mlist = reinterpret_cast<int *>(io.group_parts + io.M + 64);  // candidate indices
+  int *clist = reinterpret_cast<int *>(io.group_parts + io.M + 64) + io.M + 64;  // nonzero CTAs, per-warp slices
+  const double inv_lam = 1.0 / io.lam;
+  // 1. global minimum over the CTA heads (first CTA attaining it)
+  const int span = ((ctas + nw - 1) / nw + 31) & ~31;
+  const int w0 = warp * span, w1 = min(ctas, w0 + span);
+  double mn = dinf();
+  int bidx = 0x7fffffff;
+  double nf = 0.0;
+  for (int c = w0; c < w1; c += 32 * 4) {
+    double v[4], f[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int i = c + 32 * t + lane;
+      v[t] = i < w1 ? heads[i] : dinf();
+      f[t] = i < w1 ? heads[ctas + i] : 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      nf += f[t];
+      if (v[t] < mn) {
+        mn = v[t];
+        bidx = c + 32 * t + lane;
+      }
+    }
+  }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    const double ov = __shfl_xor_sync(kFull, mn, d);
+    const int oi = __shfl_xor_sync(kFull, bidx, d);
+    if (ov < mn || (ov == mn && oi < bidx)) {
+      mn = ov;
+      bidx = oi;
+    }
+  }
+  nf = warp_sum_d(nf);
+  if (lane == 0) {
+    misc[warp] = mn;
+    misc[16 + warp] = (double)bidx;
+    misc[32 + warp] = nf;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m0 = dinf(), NF = 0.0;
+    int b0 = 0x7fffffff;
+    for (int w = 0; w < nw; ++w) {
+      const double v = misc[w];
+      const int b = (int)misc[16 + w];
+      NF += misc[32 + w];
+      if (v < m0 || (v == m0 && b < b0)) {
+        m0 = v;
+        b0 = b;
+      }
+    }
+    misc[40] = m0;
+    misc[41] = (double)b0;
+    misc[43] = NF;
+  }
+  __syncthreads();
+  const double m0 = misc[40];
+  // 2. (all warps) CTAs with a nonzero weight, compacted in order into this
+  //    warp's slice of clist (cheap exponent pre-check; exp only near the min)
+  int wn = 0;
+  for (int c = w0; c < w1; c += 32) {
+    const int i = c + lane;
+    const double v = i < w1 ? heads[i] : dinf();
+    const double x = (v - m0) * inv_lam;
+    const bool nz = v < dinf() && x < 746.0 && exp(-x) != 0.0;
+    const unsigned bal = __ballot_sync(kFull, nz);
+    if (nz) clist[w0 + wn + __popc(bal & ((1u << lane) - 1u))] = i;
+    wn += __popc(bal);
+  }
+  if (lane == 0) misc[16 + warp] = (double)wn;
+  __syncthreads();
+  if (tid < 32) {
+    // 3. (warp 0) the candidates of those CTAs, in order: weights and Z
+    int ncand = 0;
+    double z = 0.0;
+    for (int w = 0; w < nw; ++w) {
+      const int cnt = (int)misc[16 + w] * NWC;
+      const int *cl = clist + w * span;
+      for (int k0 = 0; k0 < cnt; k0 += 32) {
+        const int k = k0 + lane;
+        int m = -1;
+        double wt = 0.0;
+        if (k < cnt) {
+          m = cl[k / NWC] * NWC + (k % NWC);
+          if (m < io.M) {
+            const double c = costs[m];
+            wt = c < dinf() ? exp(-(c - m0) * inv_lam) : 0.0;
+          }
+        }
+        const unsigned bal = __ballot_sync(kFull, wt != 0.0);
+        if (wt != 0.0) {
+          const int p = ncand + __popc(bal & ((1u << lane) - 1u));
+          mlist[p] = m;
+          wlist[p] = wt;
+        }
+        z += wt;  // lane-strided partials in candidate order
+        ncand += __popc(bal);
+      }
+    }
+    z = warp_sum_d(z);
+    if (lane == 0) {
+      const int b0 = (int)misc[41];
+      double *dst = io.rank_part;
+      dst[0] = m0;
+      dst[1] = z;
+      dst[2] = misc[43];
+      dst[3] = (b0 >= 0 && b0 < ctas) ? heads[2 * (size_t)ctas + b0] : -1.0;
+      misc[42] = (double)ncand;
+    }
+  }
+  __syncthreads();
+  if (trace_head && tid == 0) *trace_head = gtimer();
+  // 3. N = sum_m w_m eps_m over the nonzero candidates, in candidate order
+  const int ncand = (int)misc[42];
+  const ET *eps = reinterpret_cast<const ET *>(io.eps);
+  for (int e = tid; e < hn; e += nt) {
+    double acc = 0.0;
+    int k = 0;
+    for (; k + 4 <= ncand; k += 4) {
+      double a[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) a[t] = load_e<ET>(eps + (size_t)mlist[k + t] * hn + e);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) acc += wlist[k + t] * a[t];
+    }
+    for (; k < ncand; ++k) acc += wlist[k] * load_e<ET>(eps + (size_t)mlist[k] * hn + e);
+    io.rank_part[kPartHead + e] = acc;
+  }
+  __syncthreads();
+}
+
+// Per-CTA head (warp 0: min cost, non-finite count, best index of the CTA's
+// candidates; costs to `costs`), publication, and -- on the last CTA -- the
+// final merge.  Returns true on the CTA that merged.
+template <typename ET, int NWC>
+__device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t cta_m0, int hn, int cta, int ctas) {
+  const int groups = (ctas + kGroup - 1) / kGroup;
+  double *heads = io.cta_parts;  // [3][ctas]
+  double *costs = io.costs ? io.costs : io.cand_costs;
+  unsigned int *flag = reinterpret_cast<unsigned int *>(S.misc + 44);
+  if (threadIdx.x < 32) {
+    const int w = threadIdx.x;
+    const int64_t m = cta_m0 + w;
+    double c = dinf();
+    if (w < NWC && m < io.M) {
+      const double *sm = S.sums + w * 6;
+      const bool failed = S.fail[w] != 0 || S.tfail[w] != 0;
+      c = failed ? dinf() : sm[0] + sm[1] + sm[2] + sm[3] + sm[4] + S.cost[w];
+      costs[m] = c;
+      if (io.flags) io.flags[m] = failed ? 1 : 0;
+    }
+    const bool real = w < NWC && m < io.M;
+    const unsigned nfm = __ballot_sync(kFull, real && !(c < dinf()));
+    double mn = c;
+    int bi = real ? w : 0x7fffffff;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+      const double ov = __shfl_xor_sync(kFull, mn, d);
+      const int oi = __shfl_xor_sync(kFull, bi, d);
+      if (ov < mn || (ov == mn && oi < bi)) {
+        mn = ov;
+        bi = oi;
+      }
+    }
+    if (w == 0) {
+      heads[cta] = mn;
+      heads[ctas + cta] = (double)__popc(nfm);
+      heads[2 * (size_t)ctas + cta] = mn < dinf() ? (double)(io.m_offset + cta_m0 + bi) : -1.0;
+      // publication: one gpu-scope release fence + the counter atomic; the
+      // CTA taking the last ticket acquires before reading the others' heads
+      fence_acq_rel_gpu();
+      const unsigned int prev = atomicAdd(&io.counters[groups], 1u);
+      const bool last = prev == (unsigned int)(ctas - 1);
+      if (last) fence_acq_rel_gpu();
+      flag[0] = last ? 1u : 0u;
+    }
+  }
+  __syncthreads();
+  VPB_TRACE(io, 2 * ctas + 3 + (cta % 4));
+  if (flag[0] == 0u) return false;
+  VPB_TRACE(io, 2 * ctas);
+  final_merge<ET, NWC>(io, S, heads, costs, ctas, hn, io.trace ? io.trace + 2 * ctas + 13 : nullptr);
+  if (threadIdx.x == 0) io.counters[groups] = 0u;
+  VPB_TRACE(io, 2 * ctas + 1);
+  return true;
 }
 
 // Fused SMPC step: rollout -> CTA partial -> group merge -> global merge
 // [-> U*, clip, shift, re-evaluation].
-template <typename T, typename ET, int MAXJ>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 ? 2 : 1) smpc_kernel(const __grid_constant__ Prob<T> P,
-                                                           const __grid_constant__ SmpcIO io) {
+template <typename T, typename ET, int MAXJ, typename Topo>
+__global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>())
+    smpc_kernel(const __grid_constant__ Prob<T> P, const __grid_constant__ SmpcIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int ctas = gridDim.x;
-  const int groups = (ctas + kGroup - 1) / kGroup;
-  const SmemLayout L = smem_layout(P.ns, sizeof(T), groups > kGroup ? groups : kGroup);
+  const SmemLayout L = smem_layout(is_dyn_v<Topo> ? P.ns : 0, sizeof(T), 0);
   const Shared S = carve(smem_raw, L);
   Dyn<T> &D = *reinterpret_cast<Dyn<T> *>(S.dyn);
   if (threadIdx.x < 32) load_dyn<T>(P, io.dyn, D);
   __syncthreads();
-  const int64_t cta_m0 = (int64_t)blockIdx.x * NW;
+  const int64_t cta_m0 = (int64_t)blockIdx.x * smpc_nw<Topo>();
   const int hn = P.H * P.nj;
-  const int Lp = kPartHead + hn;
   const ET *eps = reinterpret_cast<const ET *>(io.eps);
-  CandOut co{nullptr, nullptr, nullptr};
-  evaluate_cta<T, ET, MAXJ>(P, D, eps, io.nominal, io.M, cta_m0, S, co);
-
-  // ---- per-candidate totals ----
-  double *tot = S.misc + 24;  // NW doubles
-  if (threadIdx.x < NW) {
-    const int w = threadIdx.x;
-    const int64_t m = cta_m0 + w;
-    double c = dinf();
-    bool failed = true;
-    if (m < io.M) {
-      const double *sm = S.sums + w * 6;
-      failed = S.fail[w] != 0 || S.tfail[w] != 0;
-      c = failed ? dinf() : sm[0] + sm[1] + sm[2] + sm[3] + sm[4] + S.cost[w];
-      if (io.costs) io.costs[m] = c;
-      if (io.flags) io.flags[m] = failed ? 1 : 0;
-    }
-    tot[w] = c;
-  }
-  __syncthreads();
-  // ---- CTA partial (fixed order over the NW candidates) ----
-  double *wt_s = S.misc + 32;  // NW weights
-  if (threadIdx.x == 0) {
-    double mn = dinf();
-    int best = -1, nonfinite = 0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) {
-      if (cta_m0 + w >= io.M) continue;
-      const double c = tot[w];
-      if (!(c < dinf())) {
-        ++nonfinite;
-        continue;
+  if constexpr (is_dyn_v<Topo>) {
+    VPB_TRACE(io, 2 * blockIdx.x);
+    CandOut co{nullptr, nullptr, nullptr};
+    evaluate_cta<T, ET, MAXJ>(P, D, eps, io.nominal, io.M, cta_m0, S, co);
+    if (!cta_reduce_and_merge<ET, smpc_nw<Topo>()>(io, S, cta_m0, hn, blockIdx.x, gridDim.x)) return;
+    if (io.finish) smpc_tail_dyn<T, MAXJ>(P, D, io.rank_part, io.nominal, io.acc, io.out, S);
+  } else {
+    if (blockIdx.x > 0) VPB_TRACE(io, 2 * (blockIdx.x - 1));
+    // One call site, three uses: state 0 -- block 0 computes the q_0
+    // prologue split over its warps into io.pro and raises the ready flag
+    // (it is an extra block: it runs beside the candidates, off the critical
+    // path); state 1 -- every warp of blocks 1.. scores its candidate;
+    // state 2 (last candidate CTA) -- U* re-evaluated, split over the warps.
+    const int warp = threadIdx.x >> 5;
+    const int cta = (int)blockIdx.x - 1, ncta = (int)gridDim.x - 1;
+    const int64_t cm0 = (int64_t)cta * smpc_nw<Topo>();
+    unsigned int *pro_ready = io.counters + (ncta + kGroup - 1) / kGroup + 1;
+    int state = blockIdx.x == 0 ? 0 : 1;
+#pragma unroll 1
+    for (;;) {
+      const int64_t m = cm0 + warp;
+      const bool cand = state == 1;
+      const ET *ctrl = (cand && m < io.M) ? eps + (size_t)m * hn : nullptr;
+      const double *nom = state == 1 ? io.nominal : (state == 2 ? io.out : nullptr);
+      fixed_candidate<T, ET, Topo>(P, D, ctrl, nom, cand ? m < io.M : true, state == 0 ? 1 : P.H,
+                                   state == 0 ? 0 : 1, cand ? 0 : warp, cand ? 1 : NWF, S.sums + warp * 6,
+                                   S.cost + warp, S.fail + warp);
+      __syncthreads();
+      if (state == 0) {
+        if (threadIdx.x < NWF) {
+          const int w = threadIdx.x;
+          io.pro[4 * w + 0] = S.sums[w * 6 + 0];
+          io.pro[4 * w + 1] = S.sums[w * 6 + 1];
+          io.pro[4 * w + 2] = (double)S.fail[w];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          fence_acq_rel_gpu();
+          atomicExch(pro_ready, 1u);
+        }
+        return;
       }
-      if (c < mn) {
-        mn = c;
-        best = w;
+      if (state == 2) break;
+      S.tfail[warp] = 0;
+      __syncthreads();
+      VPB_TRACE(io, 2 * cta + 1);
+      if (!cta_reduce_and_merge<ET, smpc_nw<Topo>()>(io, S, cm0, hn, cta, ncta)) return;
+      if (threadIdx.x == 0) {  // wait for the prologue block (normally long done)
+        while (ld_acquire_gpu(pro_ready) == 0u) __nanosleep(64);
       }
+      __syncthreads();
+      if (threadIdx.x < 32) {  // q_0 terms, summed in fixed split order
+        const int w = threadIdx.x;
+        const bool has = w < NWF;
+        const double pw = has ? __ldcg(io.pro + 4 * w + 0) : 0.0;
+        const double cw = has ? __ldcg(io.pro + 4 * w + 1) : 0.0;
+        const unsigned badm = __ballot_sync(kFull, has && __ldcg(io.pro + 4 * w + 2) != 0.0);
+        const double pose0 = warp_sum_d(pw), coll0 = warp_sum_d(cw);
+        if (w == 0) {
+          S.pro[0] = pose0;
+          S.pro[1] = coll0;
+          *pro_fail(S) = badm != 0u;
+        }
+      }
+      if (!io.finish) {
+        __syncthreads();
+        fixed_shard_fixup(S, io.M, io.costs, io.flags, io.rank_part);
+        return;
+      }
+      tail_controls(io.rank_part, io.nominal, io.acc, P.H, P.nj, io.out);
+      __syncthreads();
+      VPB_TRACE(io, 2 * ncta + 11);
+      state = 2;
     }
-    S.misc[45] = mn;
-    S.misc[46] = (double)nonfinite;
-    S.misc[47] = best >= 0 ? (double)(io.m_offset + cta_m0 + best) : -1.0;
-  }
-  __syncthreads();
-  if (threadIdx.x < NW) {
-    const int w = threadIdx.x;
-    const double c = tot[w];
-    const bool ok = (cta_m0 + w < io.M) && (c < dinf());
-    wt_s[w] = ok ? exp(-(c - S.misc[45]) / io.lam) : 0.0;
-  }
-  __syncthreads();
-  double *part = io.cta_parts + (size_t)blockIdx.x * Lp;
-  if (threadIdx.x == 0) {
-    double Zc = 0.0;
-#pragma unroll
-    for (int w = 0; w < NW; ++w) Zc += wt_s[w];
-    part[0] = S.misc[45];
-    part[1] = Zc;
-    part[2] = S.misc[46];
-    part[3] = S.misc[47];
-  }
-  {
-    double wt[NW];
-#pragma unroll
-    for (int w = 0; w < NW; ++w) wt[w] = wt_s[w];
-    for (int e = threadIdx.x; e < hn; e += blockDim.x) {
-      double ev[NW];
-#pragma unroll
-      for (int w = 0; w < NW; ++w)
-        ev[w] = (cta_m0 + w < io.M) ? load_e<ET>(eps + (size_t)(cta_m0 + w) * hn + e) : 0.0;
-      double acc = 0.0;
-#pragma unroll
-      for (int w = 0; w < NW; ++w)
-        if (wt[w] != 0.0) acc += wt[w] * ev[w];
-      part[kPartHead + e] = acc;
+    VPB_TRACE(io, 2 * ncta + 12);
+    // combine the split re-evaluation (fixed warp order) + the q_0 terms
+    if (threadIdx.x == 0) {
+      for (int a = 0; a < 5; ++a) {
+        double v = 0.0;
+        for (int w = 0; w < NWF; ++w) v += S.sums[w * 6 + a];
+        S.sums[a] = v;
+      }
+      double c = 0.0;
+      int f = 0;
+      for (int w = 0; w < NWF; ++w) {
+        c += S.cost[w];
+        f |= S.fail[w];
+      }
+      S.cost[0] = c;
+      S.fail[0] = f;
+      fixed_add_prologue(S, 0);
     }
+    __syncthreads();
+    const bool bad = *pro_fail(S) != 0;
+    const double best = bad ? dinf() : io.rank_part[0] + S.pro[0] + S.pro[1];
+    tail_output(S, io.rank_part, P.H, P.nj, best, bad ? (double)io.M : io.rank_part[2], io.out);
+    fixed_shard_fixup(S, io.M, io.costs, io.flags, nullptr);
+    VPB_TRACE(io, 2 * ncta + 2);
   }
-  // ---- group merge by the group's last CTA ----
-  __threadfence();
-  __syncthreads();
-  unsigned int *flag = reinterpret_cast<unsigned int *>(S.misc + 44);
-  const int g = blockIdx.x / kGroup;
-  const int g0 = g * kGroup;
-  const int gcount = min(kGroup, ctas - g0);
-  if (threadIdx.x == 0) {
-    const unsigned int prev = atomicAdd(&io.counters[g], 1u);
-    flag[0] = (prev == (unsigned int)(gcount - 1)) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (flag[0] == 0u) return;
-  __threadfence();
-  merge_block(io.cta_parts + (size_t)g0 * Lp, gcount, hn, io.lam, io.group_parts + (size_t)g * Lp, S.scratch,
-              S.misc);
-  if (threadIdx.x == 0) io.counters[g] = 0u;
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned int prev = atomicAdd(&io.counters[groups], 1u);
-    flag[0] = (prev == (unsigned int)(groups - 1)) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (flag[0] == 0u) return;
-  __threadfence();
-  merge_block(io.group_parts, groups, hn, io.lam, io.rank_part, S.scratch, S.misc);
-  if (threadIdx.x == 0) io.counters[groups] = 0u;
-  if (!io.finish) return;
-  __threadfence();
-  __syncthreads();
-  smpc_tail<T, MAXJ>(P, D, io.rank_part, io.nominal, io.acc, io.out, S);
 }
 
-// Multi-device finish: merge R rank partials in rank order, then the tail.
-template <typename T, int MAXJ>
-__global__ void __launch_bounds__(kThreads, 1) smpc_finish_kernel(const __grid_constant__ Prob<T> P,
-                                                                   const double *parts, int n_parts, double lam,
-                                                                   const double *nominal, const AccLimit acc,
-                                                                   double *merged, double *out, const double *dyn) {
+// Multi-device finish: merge R rank partials in rank order (their minima
+// already include the q_0 terms), then the tail.
+template <typename T, int MAXJ, typename Topo>
+__global__ void __launch_bounds__(smpc_threads<Topo>(), 1)
+    smpc_finish_kernel(const __grid_constant__ Prob<T> P, const double *parts, int n_parts, double lam,
+                       const double *nominal, const AccLimit acc, double *merged, double *out, const double *dyn) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const SmemLayout L = smem_layout(P.ns, sizeof(T), n_parts);
+  const SmemLayout L = smem_layout(is_dyn_v<Topo> ? P.ns : 0, sizeof(T), n_parts + 512);
   const Shared S = carve(smem_raw, L);
   Dyn<T> &D = *reinterpret_cast<Dyn<T> *>(S.dyn);
   if (threadIdx.x < 32) load_dyn<T>(P, dyn, D);
   __syncthreads();
-  merge_block(parts, n_parts, P.H * P.nj, lam, merged, S.scratch, S.misc);
-  __threadfence();
-  __syncthreads();
-  smpc_tail<T, MAXJ>(P, D, merged, nominal, acc, out, S);
+  merge_block(record_rows(parts, P.H * P.nj), n_parts, P.H * P.nj, lam, merged, S.scratch, S.misc);
+  if constexpr (is_dyn_v<Topo>) {
+    smpc_tail_dyn<T, MAXJ>(P, D, merged, nominal, acc, out, S);
+  } else {
+    tail_controls(merged, nominal, acc, P.H, P.nj, out);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    // pass 0: U* split over the warps; pass 1: the q_0 prologue, split
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+      double *base = pass == 0 ? S.sums : S.scratch;
+      fixed_candidate<T, double, Topo>(P, D, nullptr, pass == 0 ? out : nullptr, true, pass == 0 ? P.H : 1,
+                                       pass == 0 ? 1 : 0, warp, NWF, base + warp * 6,
+                                       (pass == 0 ? S.cost : S.scratch + 6 * NWF) + warp,
+                                       pass == 0 ? S.fail + warp : S.tfail + warp);
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      for (int a = 0; a < 5; ++a) {
+        double v = 0.0;
+        for (int w = 0; w < NWF; ++w) v += S.sums[w * 6 + a];
+        S.sums[a] = v;
+      }
+      double c = 0.0, pose0 = 0.0, coll0 = 0.0;
+      int f = 0, bad = 0;
+      for (int w = 0; w < NWF; ++w) {
+        c += S.cost[w];
+        f |= S.fail[w];
+        pose0 += S.scratch[w * 6 + 0];
+        coll0 += S.scratch[w * 6 + 1];
+        bad |= S.tfail[w];
+      }
+      S.cost[0] = c;
+      S.fail[0] = f;
+      S.pro[0] = pose0;
+      S.pro[1] = coll0;
+      *pro_fail(S) = bad;
+      fixed_add_prologue(S, 0);
+    }
+    __syncthreads();
+    tail_output(S, merged, P.H, P.nj, merged[0], merged[2], out);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -844,13 +1361,94 @@ static int build_prob(const vpb_problem *p, const vpb_field *f, Prob<T> &P) {
     P.inv_voxel = (T)(1.0 / f->voxel);
     P.outside = (T)f->outside_default;
   }
+  // derived constants of the fixed-topology path
+  FixedConsts<T> &C = P.fc;
+  const double vox = (f && f->sq) ? f->voxel : 1.0;
+  const double outside = (f && f->sq) ? f->outside_default : 0.0;
+  for (int s = 0; s < ns; ++s) {
+    const double r = p->sph_r[s];
+    const double dr = p->d_act + r;
+    C.dr[s] = (T)dr;
+    const double t = dr / vox;
+    C.thr2[s] = (T)(t * t * (1.0 + 1e-4) + 1e-12);
+    C.zero_cost[s] = (T)(p->w_env * (p->d_act - (0.0 - r)) * (p->d_act - (0.0 - r)));
+    const double go = p->d_act - (outside - r);
+    C.out_cost[s] = (T)(go > 0.0 ? p->w_env * go * go : 0.0);
+  }
+  for (int q = 0; q < p->n_pairs; ++q) {
+    const double rs = p->sph_r[p->pairs[2 * q]] + p->sph_r[p->pairs[2 * q + 1]];
+    C.rsum[q] = (T)rs;
+    C.rsum2[q] = (T)(rs * rs * (1.0 + 1e-4) + 1e-12);
+  }
+  bool diag = true;
+  int idx = 0;
+  for (int a = 0; a < 6; ++a)
+    for (int b = a; b < 6; ++b, ++idx) {
+      const double wq = a == b ? p->pose_weight[6 * a + a] : p->pose_weight[6 * a + b] + p->pose_weight[6 * b + a];
+      const double wt =
+          a == b ? p->terminal_weight[6 * a + a] : p->terminal_weight[6 * a + b] + p->terminal_weight[6 * b + a];
+      C.Wq[idx] = (T)wq;
+      C.Wt[idx] = (T)wt;
+      if (a != b && (wq != 0.0 || wt != 0.0)) diag = false;
+    }
+  C.w_diag = diag ? 1 : 0;
+  const int fn0 = P.has_field ? P.n0 : 1, fn1 = P.has_field ? P.n1 : 1, fn2 = P.has_field ? P.n2 : 1;
+  C.off2 = fn2 >= 2 ? 1 : 0;
+  C.off1 = fn1 >= 2 ? fn2 : 0;
+  C.off0 = fn0 >= 2 ? fn1 * fn2 : 0;
+  C.amax0 = (T)(fn0 >= 2 ? fn0 - 2 : 0);
+  C.amax1 = (T)(fn1 >= 2 ? fn1 - 2 : 0);
+  C.amax2 = (T)(fn2 >= 2 ? fn2 - 2 : 0);
+  C.nf0 = (T)fn0;
+  C.nf1 = (T)fn1;
+  C.nf2 = (T)fn2;
+  C.chi0 = (T)(fn0 - 1);
+  C.chi1 = (T)(fn1 - 1);
+  C.chi2 = (T)(fn2 - 1);
   return VPB_OK;
 }
 
+// VPB_GENERIC_ROLLOUT=1 forces the runtime-topology kernels (A/B parity tests).
+static bool fixed_topology_disabled() {
+  const char *e = getenv("VPB_GENERIC_ROLLOUT");
+  return e && e[0] == '1';
+}
+
+// Does the packed problem have exactly the compile-time topology `Topo`?
+static int axis_code(const double *u) {
+  if (u[1] == 0.0 && u[2] == 0.0 && (u[0] == 1.0 || u[0] == -1.0)) return u[0] > 0 ? 1 : -1;
+  if (u[0] == 0.0 && u[2] == 0.0 && (u[1] == 1.0 || u[1] == -1.0)) return u[1] > 0 ? 2 : -2;
+  if (u[0] == 0.0 && u[1] == 0.0 && (u[2] == 1.0 || u[2] == -1.0)) return u[2] > 0 ? 3 : -3;
+  return 0;
+}
+
+template <typename Topo>
+static bool topo_matches(const vpb_problem *p) {
+  if (p->n_joints != Topo::NJ || p->n_spheres != Topo::NS || p->n_pairs != Topo::NP) return false;
+  for (int j = 0; j < Topo::NJ; ++j) {
+    if (Topo::axis(j) != 0 && axis_code(p->axes + 3 * j) != Topo::axis(j)) return false;
+    if (Topo::offset_kind(j) == 1) {
+      for (int a = 0; a < 9; ++a)
+        if (p->off_r[9 * j + a] != ((a % 4 == 0) ? 1.0 : 0.0)) return false;
+      if (p->off_t[3 * j] != 0.0 || p->off_t[3 * j + 1] != 0.0) return false;
+    }
+  }
+  for (int s = 0; s < Topo::NS; ++s) {
+    if (p->sph_link[s] != Topo::link(s)) return false;
+    if (Topo::sphere_kind(s) == 1 && (p->sph_loc[3 * s] != 0.0 || p->sph_loc[3 * s + 1] != 0.0)) return false;
+  }
+  for (int q = 0; q < Topo::NP; ++q)
+    if (p->pairs[2 * q] != Topo::pair_i(q) || p->pairs[2 * q + 1] != Topo::pair_j(q)) return false;
+  return true;
+}
+
+// 0 = generic (runtime topology), 1 = TopoRobot7
+static int topo_id(const vpb_problem *p) { return topo_matches<TopoRobot7>(p) ? 1 : 0; }
+
 
 template <typename T>
-static size_t smem_bytes(const Prob<T> &P, int scratch) {
-  return smem_layout(P.ns, sizeof(T), scratch).total;
+static size_t smem_bytes(const Prob<T> &P, int scratch, int topo) {
+  return smem_layout(topo ? 0 : P.ns, sizeof(T), scratch).total;
 }
 
 template <typename K>
@@ -860,17 +1458,21 @@ static int set_smem(K kern, size_t smem) {
 }
 
 template <typename T, typename ET>
-static int launch_rollout_t(const Prob<T> &P, const RolloutIO &io, cudaStream_t s) {
-  const size_t smem = smem_bytes(P, 0);
+static int launch_rollout_t(const Prob<T> &P, const RolloutIO &io, int topo, cudaStream_t s) {
+  const size_t smem = smem_bytes(P, 0, topo);
   const unsigned grid = (unsigned)ceil_div(io.M, NW);
   if (grid == 0) return VPB_OK;
   int rc;
-  if (P.nj <= 8) {
-    auto k = rollout_kernel<T, ET, 8>;
+  if (topo == 1) {
+    auto k = rollout_kernel<T, ET, 8, TopoRobot7>;
+    if ((rc = set_smem(k, smem))) return rc;
+    k<<<grid, kThreads, smem, s>>>(P, io);
+  } else if (P.nj <= 8) {
+    auto k = rollout_kernel<T, ET, 8, TopoDyn>;
     if ((rc = set_smem(k, smem))) return rc;
     k<<<grid, kThreads, smem, s>>>(P, io);
   } else {
-    auto k = rollout_kernel<T, ET, kMaxJ>;
+    auto k = rollout_kernel<T, ET, kMaxJ, TopoDyn>;
     if ((rc = set_smem(k, smem))) return rc;
     k<<<grid, kThreads, smem, s>>>(P, io);
   }
@@ -878,17 +1480,21 @@ static int launch_rollout_t(const Prob<T> &P, const RolloutIO &io, cudaStream_t 
 }
 
 template <typename T, typename ET>
-static int launch_smpc_t(const Prob<T> &P, const SmpcIO &io, cudaStream_t s) {
-  const int64_t ctas = ceil_div(io.M, NW);
+static int launch_smpc_t(const Prob<T> &P, const SmpcIO &io, int topo, cudaStream_t s) {
+  const int64_t ctas = ceil_div(io.M, topo ? NWF : NW) + (topo ? 1 : 0);  // fixed path: + prologue block
   const int groups = (int)ceil_div(ctas, kGroup);
-  const size_t smem = smem_bytes(P, groups > kGroup ? groups : kGroup);
+  const size_t smem = smem_bytes(P, 0, topo);
   int rc;
-  if (P.nj <= 8) {
-    auto k = smpc_kernel<T, ET, 8>;
+  if (topo == 1) {
+    auto k = smpc_kernel<T, ET, 8, TopoRobot7>;
+    if ((rc = set_smem(k, smem))) return rc;
+    k<<<(unsigned)ctas, smpc_threads<TopoRobot7>(), smem, s>>>(P, io);
+  } else if (P.nj <= 8) {
+    auto k = smpc_kernel<T, ET, 8, TopoDyn>;
     if ((rc = set_smem(k, smem))) return rc;
     k<<<(unsigned)ctas, kThreads, smem, s>>>(P, io);
   } else {
-    auto k = smpc_kernel<T, ET, kMaxJ>;
+    auto k = smpc_kernel<T, ET, kMaxJ, TopoDyn>;
     if ((rc = set_smem(k, smem))) return rc;
     k<<<(unsigned)ctas, kThreads, smem, s>>>(P, io);
   }
@@ -897,15 +1503,20 @@ static int launch_smpc_t(const Prob<T> &P, const SmpcIO &io, cudaStream_t s) {
 
 template <typename T>
 static int launch_finish_t(const Prob<T> &P, const double *parts, int n_parts, double lam, const double *nominal,
-                           const AccLimit &acc, double *merged, double *out, const double *dyn, cudaStream_t s) {
-  const size_t smem = smem_bytes(P, n_parts);
+                           const AccLimit &acc, double *merged, double *out, const double *dyn, int topo,
+                           cudaStream_t s) {
+  const size_t smem = smem_bytes(P, n_parts + 512, topo);
   int rc;
-  if (P.nj <= 8) {
-    auto k = smpc_finish_kernel<T, 8>;
+  if (topo == 1) {
+    auto k = smpc_finish_kernel<T, 8, TopoRobot7>;
+    if ((rc = set_smem(k, smem))) return rc;
+    k<<<1, smpc_threads<TopoRobot7>(), smem, s>>>(P, parts, n_parts, lam, nominal, acc, merged, out, dyn);
+  } else if (P.nj <= 8) {
+    auto k = smpc_finish_kernel<T, 8, TopoDyn>;
     if ((rc = set_smem(k, smem))) return rc;
     k<<<1, kThreads, smem, s>>>(P, parts, n_parts, lam, nominal, acc, merged, out, dyn);
   } else {
-    auto k = smpc_finish_kernel<T, kMaxJ>;
+    auto k = smpc_finish_kernel<T, kMaxJ, TopoDyn>;
     if ((rc = set_smem(k, smem))) return rc;
     k<<<1, kThreads, smem, s>>>(P, parts, n_parts, lam, nominal, acc, merged, out, dyn);
   }
@@ -919,26 +1530,30 @@ static AccLimit acc_of(const vpb_problem *p) {
 }
 
 struct SmpcWs {
-  double *cta_parts, *group_parts, *rank_part;
+  double *cta_parts, *group_parts, *rank_part, *pro, *cand_costs;
   unsigned int *counters;
   size_t bytes;
 };
 
 static SmpcWs smpc_ws(void *base, int64_t M, int64_t H, int64_t n) {
-  const int64_t ctas = ceil_div(M > 0 ? M : 1, NW);
+  const int64_t ctas = ceil_div(M > 0 ? M : 1, NWF);  // the larger CTA count of the two paths
   const int64_t groups = ceil_div(ctas, kGroup);
   const int64_t L = kPartHead + H * n;
   SmpcWs w;
   char *b = reinterpret_cast<char *>(base);
   size_t o = 0;
-  w.cta_parts = reinterpret_cast<double *>(b + o);
-  o += align_up((size_t)ctas * L * 8, 256);
-  w.group_parts = reinterpret_cast<double *>(b + o);
-  o += align_up((size_t)groups * L * 8, 256);
+  w.cta_parts = reinterpret_cast<double *>(b + o);  // CTA heads [3][ctas]
+  o += align_up((size_t)ctas * 3 * 8, 256);
+  w.group_parts = reinterpret_cast<double *>(b + o);  // merge scratch: weights, candidate and CTA lists
+  o += align_up((size_t)(2 * (M + 64) + ctas + 600) * 8, 256);
+  w.cand_costs = reinterpret_cast<double *>(b + o);
+  o += align_up((size_t)(M > 0 ? M : 1) * 8, 256);
   w.rank_part = reinterpret_cast<double *>(b + o);
   o += align_up((size_t)L * 8, 256);
+  w.pro = reinterpret_cast<double *>(b + o);
+  o += align_up((size_t)NWF * 4 * 8, 256);
   w.counters = reinterpret_cast<unsigned int *>(b + o);
-  o += align_up((size_t)(groups + 1) * 4, 256);
+  o += align_up((size_t)(groups + 2) * 4, 256);  // group counters, global counter, prologue flag
   w.bytes = o;
   return w;
 }
@@ -946,6 +1561,8 @@ static SmpcWs smpc_ws(void *base, int64_t M, int64_t H, int64_t n) {
 }  // namespace vpb
 
 using namespace vpb;
+
+static unsigned long long *g_smpc_trace = nullptr;
 
 static int prob_checks(const vpb_problem *prob, int precision, int dtype) {
   VPB_REQUIRE(prob, "null problem");
@@ -977,17 +1594,23 @@ int vpb_evaluate_batch(const vpb_problem *prob, const vpb_field *field, const vo
   io.sph_out = sphere_pos;
   io.dyn = prob->dyn_state;
   cudaStream_t s = as_stream(stream);
+  // the fixed-topology kernels do not emit per-step trajectories / spheres
+  const int topo = (traj_q || sphere_pos || fixed_topology_disabled()) ? 0 : topo_id(prob);
   if (precision == VPB_PREC_F64) {
     Prob<double> P;
     if ((rc = build_prob<double>(prob, field, P))) return rc;
-    return dtype == VPB_DTYPE_F32 ? launch_rollout_t<double, float>(P, io, s) : launch_rollout_t<double, double>(P, io, s);
+    return dtype == VPB_DTYPE_F32 ? launch_rollout_t<double, float>(P, io, topo, s)
+                                  : launch_rollout_t<double, double>(P, io, topo, s);
   }
   Prob<float> P;
   if ((rc = build_prob<float>(prob, field, P))) return rc;
-  return dtype == VPB_DTYPE_F32 ? launch_rollout_t<float, float>(P, io, s) : launch_rollout_t<float, double>(P, io, s);
+  return dtype == VPB_DTYPE_F32 ? launch_rollout_t<float, float>(P, io, topo, s)
+                                : launch_rollout_t<float, double>(P, io, topo, s);
 }
 
 int64_t vpb_smpc_partial_len(int64_t H, int64_t n) { return kPartHead + H * n; }
+
+void vpb_debug_smpc_trace(unsigned long long *dev_buffer) { g_smpc_trace = dev_buffer; }
 
 size_t vpb_smpc_workspace_bytes(int64_t M, int64_t H, int64_t n) { return smpc_ws(nullptr, M, H, n).bytes + 256; }
 
@@ -1002,12 +1625,12 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   VPB_REQUIRE(eps && nominal && M >= 1, "bad arguments to the SMPC step");
   VPB_REQUIRE(prob->lam > 0.0, "temperature must be positive");
   const int64_t H = prob->horizon, n = prob->n_joints;
-  VPB_REQUIRE(M <= ((int64_t)1 << 31) * NW, "too many samples");
+  VPB_REQUIRE(M <= ((int64_t)1 << 31) * NWF, "too many samples");
   const SmpcWs w = smpc_ws(workspace, M, H, n);
   VPB_REQUIRE(workspace && workspace_bytes >= w.bytes, "workspace too small");
-  const int64_t ctas = ceil_div(M, NW);
+  const int64_t ctas = ceil_div(M, NWF);
   const int64_t groups = ceil_div(ctas, kGroup);
-  VPB_CUDA(cudaMemsetAsync(w.counters, 0, (size_t)(groups + 1) * 4, s));
+  VPB_CUDA(cudaMemsetAsync(w.counters, 0, (size_t)(groups + 2) * 4, s));
   SmpcIO io;
   memset(&io, 0, sizeof(io));
   io.eps = eps;
@@ -1021,18 +1644,24 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   io.group_parts = w.group_parts;
   io.counters = w.counters;
   io.rank_part = part_out ? part_out : w.rank_part;
+  io.pro = w.pro;
+  io.cand_costs = w.cand_costs;
   io.finish = out != nullptr;
   io.out = out;
   io.acc = acc_of(prob);
   io.dyn = prob->dyn_state;
+  io.trace = g_smpc_trace;
+  const int topo = fixed_topology_disabled() ? 0 : topo_id(prob);
   if (precision == VPB_PREC_F64) {
     Prob<double> P;
     if ((rc = build_prob<double>(prob, field, P))) return rc;
-    return dtype == VPB_DTYPE_F32 ? launch_smpc_t<double, float>(P, io, s) : launch_smpc_t<double, double>(P, io, s);
+    return dtype == VPB_DTYPE_F32 ? launch_smpc_t<double, float>(P, io, topo, s)
+                                  : launch_smpc_t<double, double>(P, io, topo, s);
   }
   Prob<float> P;
   if ((rc = build_prob<float>(prob, field, P))) return rc;
-  return dtype == VPB_DTYPE_F32 ? launch_smpc_t<float, float>(P, io, s) : launch_smpc_t<float, double>(P, io, s);
+  return dtype == VPB_DTYPE_F32 ? launch_smpc_t<float, float>(P, io, topo, s)
+                                : launch_smpc_t<float, double>(P, io, topo, s);
 }
 
 int vpb_smpc_partial(const vpb_problem *prob, const vpb_field *field, const void *eps, int dtype,
@@ -1068,15 +1697,17 @@ int vpb_smpc_finish(const vpb_problem *prob, const vpb_field *field, const doubl
   double *merged = reinterpret_cast<double *>(workspace);
   cudaStream_t s = as_stream(stream);
   const AccLimit acc = acc_of(prob);
+  const int topo = fixed_topology_disabled() ? 0 : topo_id(prob);
   if (precision == VPB_PREC_F64) {
     Prob<double> P;
     if ((rc = build_prob<double>(prob, field, P))) return rc;
     return launch_finish_t<double>(P, partials, (int)n_parts, prob->lam, nominal, acc, merged, out, prob->dyn_state,
-                                   s);
+                                   topo, s);
   }
   Prob<float> P;
   if ((rc = build_prob<float>(prob, field, P))) return rc;
-  return launch_finish_t<float>(P, partials, (int)n_parts, prob->lam, nominal, acc, merged, out, prob->dyn_state, s);
+  return launch_finish_t<float>(P, partials, (int)n_parts, prob->lam, nominal, acc, merged, out, prob->dyn_state,
+                                topo, s);
 }
 
 }  // extern "C"

@@ -15,6 +15,23 @@ constexpr int kMaxP = VPB_MAX_PAIRS;
 // Joint axis classes for the sparse Rodrigues fast paths (warp-uniform).
 enum AxisKind : int8_t { kAxisGeneral = 0, kAxisX = 1, kAxisY = 2, kAxisZ = 3 };
 
+// Per-sphere and per-pair derived constants (host-computed in T).
+template <typename T>
+struct FixedConsts {
+  T dr[kMaxS];         // d_act + r_s
+  T thr2[kMaxS];       // squared-voxel value above which the env term is certainly 0
+  T zero_cost[kMaxS];  // env cost when the containing cell is occupied (distance 0)
+  T out_cost[kMaxS];   // env cost outside the field volume
+  T rsum[kMaxP];       // r_i + r_j
+  T rsum2[kMaxP];      // upper bound of (r_i + r_j)^2 (squared pre-check)
+  T Wq[21], Wt[21];    // symmetric parts of Q and Q_H (upper triangle, row major)
+  int w_diag;          // both weights diagonal
+  int off0, off1, off2;  // corner strides along x / y / z (0 on a length-1 axis)
+  T amax0, amax1, amax2;  // max(n - 2, 0): lower interpolation corner bound
+  T nf0, nf1, nf2;        // n as T
+  T chi0, chi1, chi2;     // n - 1
+};
+
 template <typename T>
 struct Prob {
   int nj, ns, np, H;
@@ -44,6 +61,7 @@ struct Prob {
   T origin0, origin1, origin2;
   T voxel, inv_voxel, outside;
   T pi_limit;  // pi - _PI_MARGIN in T
+  FixedConsts<T> fc;  // derived constants of the compile-time-topology path
 };
 
 // Per-call state (start state and goal).  Read from a device buffer when the

@@ -53,69 +53,69 @@ __device__ __forceinline__ void box_muller_f(uint32_t a, uint32_t b, float &z0, 
   z1 = r * s;
 }
 
-__device__ __forceinline__ void box_muller(uint32_t a, uint32_t b, double &z0, double &z1) {
-  const double u1 = ((double)a + 0.5) * 2.3283064365386963e-10;  // (0,1)
-  const double u2 = ((double)b + 0.5) * 2.3283064365386963e-10;
-  const double r = sqrt(-2.0 * log(u1));
-  double s, c;
-  sincospi(2.0 * u2, &s, &c);
-  z0 = r * c;
-  z1 = r * s;
-}
 
-// One warp per sample; raw normals staged in shared memory, then smoothed.
+// Thread = (sample m, 8-step chunk c, joint j), j fastest.  Column j of
+// sample m is a Philox4x32-10 stream keyed by (seed, global m) with counter
+// (4-step chunk, j, m): each thread draws the 16 normals of steps
+// [8c - 4, 8c + 12) (neighbouring threads redraw the overlap bit-identically),
+// applies the moving average of vp/planner.py:182-196 (window <= 9, rows
+// scaled 1/sqrt(count)) and sigma_j, and writes its 8 outputs.  Everything
+// stays in registers; no shared memory, no synchronisation.
+constexpr int kChunk = 8;
+
+template <typename OT>
 __global__ void __launch_bounds__(256) sampler_kernel(const __grid_constant__ SamplerArgs A) {
-  extern __shared__ double raw[];  // [8][H*n]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t mloc = (int64_t)blockIdx.x * 8 + warp;
-  const int64_t hn = A.H * A.n;
-  double *r = raw + (size_t)warp * hn;
-  if (mloc >= A.M) return;
+  const int n = (int)A.n, H = (int)A.H;
+  const unsigned C = (unsigned)(H + kChunk - 1) / kChunk;
+  const unsigned gid = blockIdx.x * blockDim.x + threadIdx.x;  // < 2^31 (checked on the host)
+  if (gid >= (unsigned)(A.M * (int64_t)C * n)) return;
+  const unsigned mc = gid / (unsigned)n;
+  const int j = (int)(gid - mc * (unsigned)n);
+  const unsigned mq = mc / C;
+  const int c = (int)(mc - mq * C);
+  const int64_t mloc = mq;
   const int64_t mg = A.m_offset + mloc;
   const uint64_t seed = A.seed_dev ? *A.seed_dev : A.seed;
   const uint32_t k0 = (uint32_t)seed ^ (uint32_t)((uint64_t)mg * 0x9E3779B97F4A7C15ull);
   const uint32_t k1 = (uint32_t)(seed >> 32) ^ (uint32_t)((uint64_t)mg >> 32) ^ 0x85EBCA6Bu;
-  const int64_t ncalls = (hn + 3) / 4;
-  for (int64_t c = lane; c < ncalls; c += 32) {
-    const uint4 x = philox4x32_10(make_uint4((uint32_t)c, (uint32_t)mg, (uint32_t)(mg >> 32), 0x5eedu), k0, k1);
-    double z[4];
-    if (A.dtype == VPB_DTYPE_F32) {
-      float f[4];
-      box_muller_f(x.x, x.y, f[0], f[1]);
-      box_muller_f(x.z, x.w, f[2], f[3]);
+  const int h0 = c * kChunk;
+  float z[16];  // steps h0 - 4 + i
+  const int nq = (H + 3) >> 2;  // 4-step Philox chunks of the column
 #pragma unroll
-      for (int t = 0; t < 4; ++t) z[t] = f[t];
+  for (int q = 0; q < 4; ++q) {
+    const int cq = 2 * c - 1 + q;  // 4-step chunk index
+    if (cq >= 0 && cq < nq) {
+      const uint4 x = philox4x32_10(make_uint4((uint32_t)cq, (uint32_t)j, (uint32_t)mg, 0x5eedu), k0, k1);
+      box_muller_f(x.x, x.y, z[4 * q + 0], z[4 * q + 1]);
+      box_muller_f(x.z, x.w, z[4 * q + 2], z[4 * q + 3]);
     } else {
-      box_muller(x.x, x.y, z[0], z[1]);
-      box_muller(x.z, x.w, z[2], z[3]);
-    }
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (4 * c + t < hn) r[4 * c + t] = z[t];
+      for (int t = 0; t < 4; ++t) z[4 * q + t] = 0.0f;
+    }
   }
-  __syncwarp();
-  const int64_t back = (A.window - 1) / 2, fwd = A.window / 2;
-  const bool smooth = A.window > 1;
-  for (int64_t e = lane; e < hn; e += 32) {
-    const int64_t h = e / A.n, j = e - h * A.n;
-    double v;
-    if (mg == 0) {
-      v = 0.0;
-    } else if (!smooth) {
-      v = r[e];
+  const int back = (int)(A.window - 1) / 2, fwd = (int)A.window / 2;
+  const bool zero = mg == 0;  // reserved nominal sample
+  const float sig = (float)A.sigma[j];
+  OT *out = reinterpret_cast<OT *>(A.out) + ((size_t)mloc * H) * n + j;
+#pragma unroll
+  for (int t = 0; t < kChunk; ++t) {
+    const int h = h0 + t;
+    if (h >= H) break;
+    float v;
+    if (A.window > 1) {
+      float acc = 0.0f;
+      int cnt = 0;
+#pragma unroll
+      for (int d = -4; d <= 4; ++d) {
+        const bool in = d >= -back && d <= fwd && h + d >= 0 && h + d < H;
+        acc += in ? z[t + 4 + d] : 0.0f;
+        cnt += in ? 1 : 0;
+      }
+      v = acc * rsqrtf((float)cnt);
     } else {
-      const int64_t lo = h - back > 0 ? h - back : 0;
-      const int64_t hi = h + fwd + 1 < A.H ? h + fwd + 1 : A.H;
-      double acc = 0.0;
-      for (int64_t k = lo; k < hi; ++k) acc += r[k * A.n + j];
-      v = acc / sqrt((double)(hi - lo));
+      v = z[t + 4];
     }
-    v *= A.sigma[j];
-    const size_t o = (size_t)mloc * hn + e;
-    if (A.dtype == VPB_DTYPE_F32)
-      reinterpret_cast<float *>(A.out)[o] = (float)v;
-    else
-      reinterpret_cast<double *>(A.out)[o] = v;
+    out[(size_t)h * n] = (OT)(zero ? 0.0f : v * sig);
   }
 }
 
@@ -142,10 +142,15 @@ extern "C" int vpb_sample_perturbations(uint64_t seed, const uint64_t *seed_dev,
   for (int64_t j = 0; j < n; ++j) A.sigma[j] = sigma[j];
   A.out = out;
   A.dtype = dtype;
-  const size_t smem = (size_t)8 * H * n * sizeof(double);
-  VPB_REQUIRE(smem <= 200 * 1024, "horizon x dof too large for the sampler (max 3200)");
-  if (smem > 48 * 1024)
-    VPB_CUDA(cudaFuncSetAttribute(sampler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  sampler_kernel<<<(unsigned)ceil_div(M, 8), 256, smem, as_stream(stream)>>>(A);
+  VPB_REQUIRE(window >= 1 && window <= 9, "noise window must be in [1, 9]");
+  const int64_t C = (H + kChunk - 1) / kChunk;
+  const int64_t total = M * C * n;
+  VPB_REQUIRE(total < ((int64_t)1 << 31), "too many samples for one sampler launch");
+  const unsigned grid = (unsigned)ceil_div(total, 256);
+  cudaStream_t s = as_stream(stream);
+  if (dtype == VPB_DTYPE_F32)
+    sampler_kernel<float><<<grid, 256, 0, s>>>(A);
+  else
+    sampler_kernel<double><<<grid, 256, 0, s>>>(A);
   return check_launch("sampler_kernel");
 }

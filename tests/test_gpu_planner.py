@@ -353,3 +353,56 @@ def test_fused_step_equals_partial_finish_and_graph(pk, precision):
         res2 = g.step(state2, goal, None, 7)
         direct2 = pl.smpc_step(state2, goal, field, None, 7)
         np.testing.assert_array_equal(res2.command, direct2.command)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_fixed_topology_equals_generic(pk, precision, monkeypatch):
+    """The compile-time-topology kernels (robot_7dof) and the runtime-topology
+    kernels agree on costs, terms, flags and the fused SMPC step, on a field
+    with obstacles near the arm (collision + self terms active) and on the
+    collision-free board scene, H below, at and above one warp."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200 import scene
+    from paper_2512_22575_b200.geometry import RigidTransform
+
+    chain, model = config.robot_7dof()
+    grid = mapping.VoxelGrid((-0.8, -0.8, 0.0), 0.04, (40, 40, 32))
+    occ = np.zeros((40, 40, 32), bool)
+    occ[22:26, 18:24, 8:20] = True
+    occ[10:13, 25:28, 14:16] = True
+    grid.set_log_odds(np.where(occ, 3.5, 0.0))
+    near = mapping.edt_3d(grid, outside_default=0.8)
+    origin, voxel, bocc = scene.reach_static_occupancy()
+    g2 = mapping.VoxelGrid(origin, voxel, bocc.shape)
+    g2.set_log_odds(np.where(bocc, 3.5, 0.0))
+    board = mapping.edt_3d(g2, outside_default=0.8)
+    rtol = 1e-4 if precision == "fp32" else 1e-11
+    for field, (m, h) in ((near, (517, 20)), (board, (1024, 32)), (near, (300, 45)), (None, (64, 7))):
+        params = config.planner_params(7, {"samples": m, "horizon": h})
+        pl = planner.Planner(chain, model, params, precision)
+        state = robot.JointState(np.linspace(-0.6, 0.8, 7), np.linspace(-0.3, 0.3, 7), np.zeros(7))
+        goal = RigidTransform.from_vec7([0.35, -0.25, 0.6, 0.9, 0.1, 0.3, -0.2])
+        nom = torch.from_numpy(0.3 * np.sin(np.arange(h * 7)).reshape(h, 7)).cuda()
+        eps = pl.sample_device(5) * 3.0
+        out = {}
+        for mode in ("0", "1"):
+            monkeypatch.setenv("VPB_GENERIC_ROLLOUT", mode)
+            c, t, f, *_ = pl.evaluate_device(state, goal, field, eps, nom)
+            step = pl.smpc_step_device(state, goal, field, nom, eps)
+            out[mode] = (c.cpu().numpy(), t.cpu().numpy(), f.cpu().numpy(), step.cpu().numpy())
+        (c0, t0, f0, s0), (c1, t1, f1, s1) = out["0"], out["1"]
+        np.testing.assert_array_equal(f0, f1)
+        ok = f1 == 0
+        assert ok.sum() > m // 2
+        if precision == "fp32":
+            _fp32_close(c0[ok], t0[ok], c1[ok], t1[ok], f"fixed vs generic m={m} h={h}")
+        else:
+            np.testing.assert_allclose(c0[ok], c1[ok], rtol=rtol)
+            np.testing.assert_allclose(t0[ok], t1[ok], rtol=rtol, atol=1e-12)
+        if field is near:
+            assert (t1[ok, 1] > 0).mean() > 0.05, "collision term inactive: the test would not cover it"
+        hn = h * 7
+        assert s0[-1] == s1[-1]  # best sample index
+        np.testing.assert_allclose(s0[2 * hn + 7 + 7], s1[2 * hn + 7 + 7], rtol=rtol)  # best cost
+        if precision == "fp64":  # fp32 weights at lam = 0.05 amplify 1e-6 cost noise; fp64 compares U*
+            np.testing.assert_allclose(s0, s1, rtol=1e-9, atol=1e-9)

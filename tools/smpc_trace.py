@@ -1,0 +1,68 @@
+"""Phase timeline of one fused SMPC step (C3 scene): per-CTA start / candidates
+done (%globaltimer), merge and tail stamps.  Prints a JSON summary."""
+import argparse
+import json
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--samples", type=int, default=4096)
+    ap.add_argument("--horizon", type=int, default=32)
+    a = ap.parse_args()
+    import bench
+    from paper_2512_22575_b200 import _device as D
+    from paper_2512_22575_b200 import _lib
+
+    args = argparse.Namespace(samples=a.samples, horizon=a.horizon, grid=256, precision="fp32")
+    S = bench.make_scene(args, torch.device("cuda", 0))
+    pl, st, goal, field = S["planner"], S["state"], S["goal"], S["field"]
+    nom = torch.zeros((a.horizon, 7), dtype=torch.float64, device="cuda")
+    eps = pl.sample_device(3)
+    ctas = (a.samples + 3) // 4  # fixed-topology path: 4 candidates per CTA
+    buf = torch.zeros(2 * ctas + 32, dtype=torch.int64, device="cuda")
+    for _ in range(5):
+        pl.smpc_step_device(st, goal, field, nom, eps)
+    torch.cuda.synchronize()
+    lib = _lib.load()
+    res = []
+    for _ in range(5):
+        buf.zero_()
+        lib.vpb_debug_smpc_trace(D.ptr(buf))
+        pl.smpc_step_device(st, goal, field, nom, eps)
+        torch.cuda.synchronize()
+        lib.vpb_debug_smpc_trace(None)
+        t = buf.cpu().numpy().astype(np.float64)
+        t0 = t[0:2 * ctas:2].min()
+        start = t[0:2 * ctas:2] - t0
+        done = t[1:2 * ctas:2] - t0
+        res.append({
+            "cta_start_us": [float(np.percentile(start, p)) / 1e3 for p in (0, 50, 90, 100)],
+            "cta_eval_us_p50": float(np.median(done - start)) / 1e3,
+            "cta_done_us": [float(np.percentile(done, p)) / 1e3 for p in (0, 50, 90, 100)],
+            "group_merges_done_us": (t[2 * ctas] - t0) / 1e3,
+            "global_merge_done_us": (t[2 * ctas + 1] - t0) / 1e3,
+            "step_done_us": (t[2 * ctas + 2] - t0) / 1e3,
+            "some_partials_written_us": [(x - t0) / 1e3 for x in t[2 * ctas + 3:2 * ctas + 7]],
+            "some_group_merge_starts_us": [(x - t0) / 1e3 for x in t[2 * ctas + 7:2 * ctas + 11]],
+            "u_star_done_us": (t[2 * ctas + 11] - t0) / 1e3,
+            "reeval_done_us": (t[2 * ctas + 12] - t0) / 1e3,
+            "global_merge_head_done_us": (t[2 * ctas + 13] - t0) / 1e3,
+            "merge_argmin_local_us": (t[2 * ctas + 14] - t0) / 1e3,
+            "merge_compaction_done_us": (t[2 * ctas + 15] - t0) / 1e3,
+            "merge2": [(t[2 * ctas + k] - t0) / 1e3 for k in (20, 22, 23, 21, 24)],
+            "slowest_ctas": [int(i) for i in np.argsort(done)[-6:]],
+            "done_by_cta_decile_us": [float(np.median(d)) / 1e3 for d in np.array_split(done, 10)],
+        })
+    print(json.dumps(res[-1], indent=1))
+
+
+if __name__ == "__main__":
+    main()
