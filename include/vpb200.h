@@ -4,7 +4,7 @@
  * Every entry point takes plain pointers and sizes (no torch types).  Pointers
  * marked (dev) are CUDA device pointers owned by the caller; (host) pointers
  * are read during the call only.  `stream` is a cudaStream_t (NULL = legacy
- * default stream).  Nothing here allocates device memory: scratch is passed in
+ * default stream).  Nothing here allocates device memory (except SMPC sessions): scratch is passed in
  * as a caller-owned workspace whose size the matching *_workspace_bytes()
  * function reports.  Every function returns VPB_OK (0) or an error code;
  * vpb_last_error() describes the most recent failure on the calling thread.
@@ -168,6 +168,10 @@ typedef struct {
    * f64; when set it overrides q0/qd0/goal_* so a captured CUDA graph can be
    * replayed after one small host->device copy. */
   const double *dyn_state;
+  /* (dev, optional) device location holding the distance-field pointer; when
+   * set it overrides field->sq (same box / dims / origin), so a captured step
+   * follows a field that is rebuilt into a new buffer every map update. */
+  const float *const *field_sq_dev;
 } vpb_problem;
 
 #define VPB_PREC_F32 0 /* production: fp32 arithmetic, fp64 cost sums */
@@ -228,7 +232,9 @@ int vpb_smpc_partial(const vpb_problem *prob, const vpb_field *field,
  * shifted warm start and the M = 1 re-evaluation of U* (vp/planner.py:
  * 614-629).  out (dev) layout (vpb_smpc_out_len doubles):
  *   [U* (H*n), command (n), next_nominal (H*n), weighted_cost, terms[6],
- *    best_cost, Z, nonfinite_count, best_index]
+ *    best_cost, Z, nonfinite_count, best_index, e_pos, e_ori]
+ * (e_pos / e_ori: end-effector errors at the start state, vp/planner.py:
+ * 620-629; filled by vpb_ee_errors on the host, NaN from the device step)
  * (weighted_cost = +inf when the re-evaluation hits the log singularity). */
 int64_t vpb_smpc_out_len(int64_t H, int64_t n);
 int vpb_smpc_step(const vpb_problem *prob, const vpb_field *field,
@@ -257,6 +263,40 @@ int vpb_sample_perturbations(uint64_t seed, const uint64_t *seed_dev,
                              int64_t m_offset, int64_t M, int64_t H, int64_t n,
                              int64_t window, const double *sigma, int dtype,
                              void *out, void *stream);
+
+/* ------------------------------------------------------------------------ */
+/* SMPC session: one host call per step (vp/planner.py:594-630 with host     */
+/* buffers).  Owns pinned staging, device buffers and a captured CUDA graph  */
+/* (H2D of the per-call block -> sampler -> fused step -> D2H).              */
+/* ------------------------------------------------------------------------ */
+typedef struct vpb_smpc_session vpb_smpc_session;
+
+/* Length of the step output (same layout as vpb_smpc_step's `out`). */
+int64_t vpb_smpc_session_out_len(int64_t H, int64_t n);
+/* prob/field (host structs, copied; prob->q0/qd0/goal_* and dyn_state are
+ * ignored), M samples, noise window and sigma (n) of the sampler, precision.
+ * The field's box, dims, origin and voxel are fixed for the session; its
+ * device buffer may change per step (vpb_smpc_session_step's field_sq). */
+int vpb_smpc_session_create(const vpb_problem *prob, const vpb_field *field, int64_t M, int64_t window,
+                            const double *sigma, int precision, vpb_smpc_session **out);
+/* One step: q0, qd0 (n), goal_r (9, row major), goal_t (3), nominal (H x n,
+ * NULL = zeros) and the seed are host inputs; field_sq (dev, NULL = the
+ * creation-time buffer); out (host, vpb_smpc_session_out_len doubles).  The
+ * graph is replayed on `stream` (NULL = the session's own stream), so it is
+ * ordered after the work that produced the field; the call returns when the
+ * step is complete. */
+int vpb_smpc_session_step(vpb_smpc_session *session, const double *q0, const double *qd0, const double *goal_r,
+                          const double *goal_t, const double *nominal, uint64_t seed, const float *field_sq,
+                          double *out, void *stream);
+int vpb_smpc_session_destroy(vpb_smpc_session *session);
+
+/* Step diagnostics on the host (vp/planner.py:620-629): end-effector position
+ * error and quaternion angle to the goal at configuration q0 (n), in double,
+ * following forward_kinematics (vp/robot.py:172-189) and quaternion_angle
+ * (vp/geometry.py:368-371).  The step outputs leave their e_pos / e_ori slots
+ * to this function (the session fills them). */
+int vpb_ee_errors(const vpb_problem *prob, const double *q0, const double *goal_r, const double *goal_t,
+                  double *e_pos, double *e_ori);
 
 /* ------------------------------------------------------------------------ */
 /* Diagnostics                                                               */

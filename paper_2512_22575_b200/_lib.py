@@ -75,6 +75,7 @@ class VpbProblem(ctypes.Structure):
         ("q0", _d * MAX_JOINTS), ("qd0", _d * MAX_JOINTS),
         ("w_env", _d), ("w_self", _d), ("w_q", _d), ("w_qd", _d), ("w_qdd", _d),
         ("w_s", _d), ("w_ns", _d), ("d_act", _d), ("lam", _d), ("dyn_state", _p),
+        ("field_sq_dev", _p),
     ]
 
 
@@ -112,6 +113,12 @@ SIGNATURES = {
     "vpb_sample_perturbations": (ctypes.c_int, [ctypes.c_uint64, _p, _i64, _i64, _i64, _i64, _i64, _p,
                                                 ctypes.c_int, _p, _p]),
     "vpb_debug_smpc_trace": (None, [_p]),
+    "vpb_smpc_session_out_len": (_i64, [_i64, _i64]),
+    "vpb_smpc_session_create": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _i64, _i64, _p, ctypes.c_int,
+                                               _P(_p)]),
+    "vpb_smpc_session_step": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, ctypes.c_uint64, _p, _p, _p]),
+    "vpb_smpc_session_destroy": (ctypes.c_int, [_p]),
+    "vpb_ee_errors": (ctypes.c_int, [_P(VpbProblem), _p, _p, _p, _p, _p]),
 }
 
 _lib: ctypes.CDLL | None = None

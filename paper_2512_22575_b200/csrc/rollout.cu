@@ -111,7 +111,7 @@ __host__ __device__ inline SmemLayout smem_layout(int ns, size_t tsize, int scra
   L.tfail = o;
   o = al16(o + (size_t)NW * 4);
   L.dyn = o;
-  o = al16(o + (size_t)(2 * kMaxJ + 12) * tsize);
+  o = al16(o + (tsize == 8 ? sizeof(Dyn<double>) : sizeof(Dyn<float>)));
   L.pro = o;  // q_0 terms of the fixed-topology path (see pro_fail)
   o = al16(o + 8 * 8);
   L.misc = o;  // 32 doubles of reduction scratch + flags
@@ -138,6 +138,7 @@ __device__ __forceinline__ void load_dyn(const Prob<T> &P, const double *dyn, Dy
     else if (i < 2 * kMaxJ + 9) D.goal_r[i - 2 * kMaxJ] = v;
     else D.goal_t[i - 2 * kMaxJ - 9] = v;
   }
+  if (lane == 0) D.sq = P.sq_dev ? *P.sq_dev : P.sq;
 }
 
 struct CandOut {
@@ -275,9 +276,9 @@ __device__ __forceinline__ void candidate_warp(const Prob<T> &P, const Dyn<T> &D
         for (int s0 = 0; s0 < ns; s0 += 2) {
           Query<T> Qa, Qb;
           const bool hb = s0 + 1 < ns;
-          query_issue<T>(P, cen[(3 * s0) * 32], cen[(3 * s0 + 1) * 32], cen[(3 * s0 + 2) * 32], Qa);
+          query_issue<T>(P, D.sq, cen[(3 * s0) * 32], cen[(3 * s0 + 1) * 32], cen[(3 * s0 + 2) * 32], Qa);
           const int s1 = hb ? s0 + 1 : s0;
-          query_issue<T>(P, cen[(3 * s1) * 32], cen[(3 * s1 + 1) * 32], cen[(3 * s1 + 2) * 32], Qb);
+          query_issue<T>(P, D.sq, cen[(3 * s1) * 32], cen[(3 * s1 + 1) * 32], cen[(3 * s1 + 2) * 32], Qb);
           const T da = query_finish<T>(P, Qa);
           const T ga = P.d_act - (da - P.sph_r[s0]);
           if (ga > T(0)) coll += P.w_env * ga * ga;
@@ -821,6 +822,7 @@ __device__ __forceinline__ void tail_output(const Shared &S, const double *part,
   out[base + 8] = part[1];    // Z
   out[base + 9] = nonfinite;  // non-finite sample count
   out[base + 10] = part[3];   // best sample index
+  out[base + 11] = out[base + 12] = __longlong_as_double(0x7ff8000000000000ll);  // e_pos / e_ori: host
 }
 
 // Generic path tail: U*, then its M = 1 re-evaluation on warps 0 and NW.
@@ -1347,6 +1349,7 @@ static int build_prob(const vpb_problem *p, const vpb_field *f, Prob<T> &P) {
     VPB_REQUIRE(f->n[0] >= 1 && f->n[1] >= 1 && f->n[2] >= 1, "empty field");
     VPB_REQUIRE(f->n[0] * f->n[1] * f->n[2] < ((int64_t)1 << 40), "field too large");
     P.sq = f->sq;
+    P.sq_dev = p->field_sq_dev;
     P.has_field = 1;
     P.n0 = (int)f->n[0];
     P.n1 = (int)f->n[1];
@@ -1614,7 +1617,7 @@ void vpb_debug_smpc_trace(unsigned long long *dev_buffer) { g_smpc_trace = dev_b
 
 size_t vpb_smpc_workspace_bytes(int64_t M, int64_t H, int64_t n) { return smpc_ws(nullptr, M, H, n).bytes + 256; }
 
-int64_t vpb_smpc_out_len(int64_t H, int64_t n) { return 2 * H * n + n + 11; }
+int64_t vpb_smpc_out_len(int64_t H, int64_t n) { return 2 * H * n + n + 13; }
 
 static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const void *eps, int dtype,
                        const double *nominal, int64_t M, int64_t m_offset, int precision, double *costs,

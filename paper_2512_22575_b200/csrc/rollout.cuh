@@ -55,6 +55,7 @@ struct Prob {
   T w_env, w_self, w_q, w_qd, w_qdd, w_s, w_ns, d_act;
   // distance field (vp/mapping.py:556-583)
   const float *sq;
+  const float *const *sq_dev;  // optional indirection (vpb_problem.field_sq_dev)
   int n0, n1, n2;
   int has_field;
   T lo0, lo1, lo2;
@@ -72,6 +73,7 @@ template <typename T>
 struct Dyn {
   T q0[kMaxJ], qd0[kMaxJ];
   T goal_r[9], goal_t[3];
+  const float *sq;  // distance field of this launch (P.sq or *P.sq_dev)
 };
 
 template <typename T>
@@ -104,7 +106,7 @@ struct Query {
 };
 
 template <typename T>
-__device__ __forceinline__ void query_issue(const Prob<T> &P, T px, T py, T pz, Query<T> &Q) {
+__device__ __forceinline__ void query_issue(const Prob<T> &P, const float *sq, T px, T py, T pz, Query<T> &Q) {
   T g0, g1, g2;
   if constexpr (sizeof(T) == 8) {
     g0 = (px - P.origin0) / P.voxel - P.lo0;
@@ -132,7 +134,6 @@ __device__ __forceinline__ void query_issue(const Prob<T> &P, T px, T py, T pz, 
   Q.f0 = c0 - T(a0);
   Q.f1 = c1 - T(a1);
   Q.f2 = c2 - T(a2);
-  const float *sq = P.sq;
   const size_t r00 = ((size_t)a0 * n1 + a1) * n2, r01 = ((size_t)a0 * n1 + b1) * n2;
   const size_t r10 = ((size_t)b0 * n1 + a1) * n2, r11 = ((size_t)b0 * n1 + b1) * n2;
   Q.v0 = __ldg(sq + r00 + a2);

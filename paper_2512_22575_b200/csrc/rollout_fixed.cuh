@@ -128,7 +128,8 @@ __device__ __forceinline__ void fixed_link(const Prob<T> &P, T q, T R[9], T t[3]
 // (the reference's b = min(a + 1, n - 1) gives the same value: at the upper
 // border its weight on b is 0 and ours puts weight 1 on the same voxel).
 template <typename T>
-__device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C, int s, T px, T py, T pz) {
+__device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C, const float *sq, int s, T px, T py,
+                                      T pz) {
   T g0, g1, g2;
   if constexpr (sizeof(T) == 8) {
     g0 = (px - P.origin0) / P.voxel - P.lo0;
@@ -152,7 +153,7 @@ __device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C,
   a2 = a2 > C.amax2 ? C.amax2 : a2;
   const T f0 = c0 - a0, f1 = c1 - a1, f2 = c2 - a2;  // in [0, 1]
   const int i0 = (int)a0, i1 = (int)a1, i2 = (int)a2;
-  const float *p = P.sq + ((i0 * P.n1 + i1) * P.n2 + i2);
+  const float *p = sq + ((i0 * P.n1 + i1) * P.n2 + i2);
   const float v0 = __ldg(p), v1 = __ldg(p + C.off2);
   const float *py_ = p + C.off1;
   const float v2 = __ldg(py_), v3 = __ldg(py_ + C.off2);
@@ -234,7 +235,7 @@ __device__ __forceinline__ bool fixed_config(const Prob<T> &P, const FixedConsts
           cy[s] = fma(R[3], lx, fma(R[4], ly, fma(R[5], lz, t[1])));
           cz[s] = fma(R[6], lx, fma(R[7], ly, fma(R[8], lz, t[2])));
         }
-        if (spheres && P.has_field && ((W.smask >> s) & 1u)) env += env_cost<T>(P, C, s, cx[s], cy[s], cz[s]);
+        if (spheres && P.has_field && ((W.smask >> s) & 1u)) env += env_cost<T>(P, C, D.sq, s, cx[s], cy[s], cz[s]);
       }
     });
   });

@@ -23,9 +23,9 @@ from . import _device as D
 from ._lib import (DTYPE_F32, DTYPE_F64, MAX_JOINTS, MAX_PAIRS, MAX_SPHERES, PREC_F32, PREC_F64, VpbField,
                    VpbProblem, check, fill, load)
 from .errors import DegenerateRotation, DimensionMismatch, WeightMismatch
-from .geometry import RigidTransform, quaternion_angle
+from .geometry import RigidTransform
 from .mapping import DistanceField, MapSnapshot
-from .robot import JointState, KinematicChain, SphereModel, forward_kinematics
+from .robot import JointState, KinematicChain, SphereModel
 
 TERM_NAMES = ("pose", "collision", "limits", "smoothness", "nullspace", "terminal")
 
@@ -225,6 +225,7 @@ class Planner:
         self.device = D.device(device)
         self._acc_limits = chain.acceleration_limits()
         self._base = pack_problem(chain, model, params)
+        self._sessions: dict = {}
 
     def problem(self, state: JointState | None, goal: RigidTransform | None, horizon: int | None = None,
                 dyn: torch.Tensor | None = None) -> VpbProblem:
@@ -375,25 +376,31 @@ class Planner:
         return out
 
     def unpack_step(self, out_host: np.ndarray, state: JointState, goal: RigidTransform, h: int) -> StepResult:
+        """StepResult from the packed step output (vpb_smpc_out_len doubles;
+        e_pos / e_ori come from the device, vp/planner.py:620-629)."""
         n = self.chain.dof
         hn = h * n
-        u_star = out_host[:hn].reshape(h, n)
-        command = out_host[hn:hn + n].copy()
-        next_nominal = out_host[hn + n:2 * hn + n].reshape(h, n).copy()
         base = 2 * hn + n
         wcost = float(out_host[base])
-        terms = out_host[base + 1:base + 7]
-        best, nonfinite = float(out_host[base + 7]), float(out_host[base + 9])
-        if nonfinite > 0 or not math.isfinite(wcost):
+        if out_host[base + 9] > 0 or not math.isfinite(wcost):
             raise DegenerateRotation("a sample reached a pose error with rotation angle at pi")
-        del u_star
-        ee = forward_kinematics(self.chain, state.q)[-1]
+        terms = out_host[base + 1:base + 7]
+        if not math.isfinite(out_host[base + 11]):  # device-step output: diagnostics on the host
+            q0 = np.ascontiguousarray(state.q, dtype=np.float64)
+            gr = np.ascontiguousarray(goal.rotation.matrix, dtype=np.float64)
+            gt = np.ascontiguousarray(goal.translation, dtype=np.float64)
+            e = np.zeros(2)
+            check(load().vpb_ee_errors(self._base, D.host_ptr(q0), D.host_ptr(gr), D.host_ptr(gt), D.host_ptr(e[:1]),
+                                       D.host_ptr(e[1:])), "ee_errors")
+            out_host = out_host.copy()
+            out_host[base + 11:base + 13] = e
         diag = StepDiagnostics(
-            best_cost=best, weighted_cost=wcost, breakdown=CostBreakdown(*[float(t) for t in terms]),
-            e_pos=float(np.linalg.norm(ee.translation - goal.translation)),
-            e_ori=quaternion_angle(ee.rotation.to_quaternion(), goal.rotation.to_quaternion()),
+            best_cost=float(out_host[base + 7]), weighted_cost=wcost,
+            breakdown=CostBreakdown(*[float(t) for t in terms]),
+            e_pos=float(out_host[base + 11]), e_ori=float(out_host[base + 12]),
         )
-        return StepResult(command=command, next_nominal=next_nominal, diagnostics=diag)
+        return StepResult(command=out_host[hn:hn + n].copy(),
+                          next_nominal=out_host[hn + n:2 * hn + n].reshape(h, n).copy(), diagnostics=diag)
 
     def smpc_step(self, state: JointState, goal: RigidTransform, snap, nominal, rng_seed: int,
                   perturbations=None) -> StepResult:
@@ -406,15 +413,26 @@ class Planner:
         nom = self.zero_nominal() if nominal is None else np.asarray(nominal, dtype=float)
         if nom.shape != (h, n):
             raise DimensionMismatch(f"nominal must be {(h, n)}, got {nom.shape}")
+        if perturbations is None:  # the production path: one native call per step
+            return self.session(snap).step(state, goal, nom, rng_seed, snap)
         nom_dev = _as_device(nom, self.device, torch.float64)
-        if perturbations is None:
-            eps_dev = self.sample_device(rng_seed)
-        else:
-            eps_dev = _as_device(perturbations, self.device, self._eps_dtype)
-            if tuple(eps_dev.shape) != (eps_dev.shape[0], h, n):
-                raise DimensionMismatch("perturbations must be (M, H, n)")
+        eps_dev = _as_device(perturbations, self.device, self._eps_dtype)
+        if tuple(eps_dev.shape) != (eps_dev.shape[0], h, n):
+            raise DimensionMismatch("perturbations must be (M, H, n)")
         out = self.smpc_step_device(state, goal, snap, nom_dev, eps_dev)
         return self.unpack_step(out.cpu().numpy(), state, goal, h)
+
+    def session(self, snap, samples: int | None = None) -> "SmpcSession":
+        """The cached native step session for this field geometry."""
+        f = _field_of(snap)
+        m = int(samples or self.params.samples)
+        key = (m, None if f is None else (tuple(f.volume.lo), f.volume.shape, tuple(np.asarray(f.origin).tolist()),
+                                         float(f.voxel_size), float(f.outside_default), str(f.sq_device.device)))
+        sess = self._sessions.get(key)
+        if sess is None:
+            sess = SmpcSession(self, snap, m)
+            self._sessions[key] = sess
+        return sess
 
     def integrate(self, state: JointState, command: np.ndarray) -> JointState:
         """vp/planner.py:632-636."""
@@ -558,3 +576,58 @@ class SmpcGraph:
         self.graph.replay()
         torch.cuda.current_stream(self.pl.device).synchronize()
         return self.pl.unpack_step(self.host_out.numpy().copy(), state, goal, self.h)
+
+
+class SmpcSession:
+    """Native single-device step (``vpb_smpc_session_*``): the per-call block
+    goes to pinned memory, one captured CUDA graph runs H2D -> sampler ->
+    fused step -> D2H on the caller's stream, and the host reads the packed
+    result.  The field geometry is fixed per session; its buffer may change
+    from step to step (the mapper rebuilds the EDT into a new tensor)."""
+
+    def __init__(self, planner: Planner, snap, samples: int):
+        self.pl = planner
+        p = planner.params
+        self.h, self.n, self.m = p.horizon, planner.chain.dof, int(samples)
+        L = load()
+        self._lib = L
+        P = planner.problem(None, None)
+        self._sigma = np.ascontiguousarray(np.broadcast_to(np.asarray(p.sigma, dtype=float), (self.n,)))
+        handle = ctypes.c_void_p()
+        torch.cuda.set_device(planner.device)
+        check(L.vpb_smpc_session_create(P, _field_struct(snap), self.m, p.noise_window, D.host_ptr(self._sigma),
+                                        planner._prec, ctypes.byref(handle)), "smpc_session_create")
+        self._h = handle
+        self.out = np.zeros(int(L.vpb_smpc_session_out_len(self.h, self.n)))
+        self._q0 = np.zeros(self.n)
+        self._qd0 = np.zeros(self.n)
+        self._gr = np.zeros(9)
+        self._gt = np.zeros(3)
+
+    def step(self, state: JointState, goal: RigidTransform, nominal: np.ndarray, rng_seed: int, snap) -> StepResult:
+        n = self.n
+        q0 = np.asarray(state.q, dtype=np.float64).reshape(-1)
+        qd0 = np.asarray(state.qd, dtype=np.float64).reshape(-1)
+        if q0.shape != (n,) or qd0.shape != (n,):
+            raise DimensionMismatch("state does not match the chain's dof")
+        self._q0[:] = q0
+        self._qd0[:] = qd0
+        self._gr[:] = np.asarray(goal.rotation.matrix, dtype=np.float64).reshape(-1)
+        self._gt[:] = np.asarray(goal.translation, dtype=np.float64).reshape(-1)
+        nom = np.ascontiguousarray(nominal, dtype=np.float64)
+        f = _field_of(snap)
+        sq = D.ptr(f.sq_device) if f is not None else None
+        check(self._lib.vpb_smpc_session_step(self._h, D.host_ptr(self._q0), D.host_ptr(self._qd0),
+                                              D.host_ptr(self._gr), D.host_ptr(self._gt), D.host_ptr(nom),
+                                              int(rng_seed) & 0xFFFFFFFFFFFFFFFF, sq, D.host_ptr(self.out),
+                                              D.stream(self.pl.device)), "smpc_session_step")
+        return self.pl.unpack_step(self.out, state, goal, self.h)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.vpb_smpc_session_destroy(h)
+            except Exception:  # interpreter shutdown
+                pass
+            self._h = None

@@ -59,7 +59,7 @@ def test_pure_host_entry_points(lib):
     assert lib.vpb_occ_words(i64x3((4, 5, 33))) == 4 * 5 * 2
     assert lib.vpb_edt3d_workspace_bytes(i64x3((8, 8, 8))) >= 8 * 8 * 8 * 6
     assert lib.vpb_smpc_partial_len(32, 7) == 4 + 224
-    assert lib.vpb_smpc_out_len(32, 7) == 2 * 224 + 7 + 11
+    assert lib.vpb_smpc_out_len(32, 7) == 2 * 224 + 7 + 13
 
 
 def test_struct_layout_matches_header(lib):
@@ -132,3 +132,29 @@ def test_reference_shim_packs_like_planner():
             assert list(a) == list(b), name
         else:
             assert a == b, name
+
+
+def test_host_ee_errors_vs_reference_golden():
+    """vpb_ee_errors (host C, no GPU) reproduces the reference's smpc_step
+    diagnostics e_pos / e_ori (vp/planner.py:620-629) from the golden steps."""
+    import ctypes
+
+    import numpy as np
+
+    from conftest import load_golden
+    from paper_2512_22575_b200 import _lib, config, planner
+
+    lib = _lib.load()
+    g = load_golden("softmin")
+    chain, model = config.robot_7dof()
+    P = planner.pack_problem(chain, model, config.planner_params(7))
+    for j in range(int(g["st_count"])):
+        q0 = np.ascontiguousarray(g[f"st_q0_{j}"], dtype=np.float64)
+        gr = np.ascontiguousarray(g[f"st_goal_r_{j}"], dtype=np.float64)
+        gt = np.ascontiguousarray(g[f"st_goal_t_{j}"], dtype=np.float64)
+        ep, eo = ctypes.c_double(), ctypes.c_double()
+        ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        assert lib.vpb_ee_errors(P, ptr(q0), ptr(gr), ptr(gt), ctypes.byref(ep), ctypes.byref(eo)) == 0
+        diag = g[f"st_diag_{j}"]
+        np.testing.assert_allclose(ep.value, diag[2], rtol=1e-12)
+        np.testing.assert_allclose(eo.value, diag[3], rtol=1e-9, atol=1e-12)

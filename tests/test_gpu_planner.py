@@ -402,7 +402,50 @@ def test_fixed_topology_equals_generic(pk, precision, monkeypatch):
         if field is near:
             assert (t1[ok, 1] > 0).mean() > 0.05, "collision term inactive: the test would not cover it"
         hn = h * 7
-        assert s0[-1] == s1[-1]  # best sample index
-        np.testing.assert_allclose(s0[2 * hn + 7 + 7], s1[2 * hn + 7 + 7], rtol=rtol)  # best cost
+        base = 2 * hn + 7
+        assert s0[base + 10] == s1[base + 10]  # best sample index
+        np.testing.assert_allclose(s0[base + 7], s1[base + 7], rtol=rtol)  # best cost
         if precision == "fp64":  # fp32 weights at lam = 0.05 amplify 1e-6 cost noise; fp64 compares U*
-            np.testing.assert_allclose(s0, s1, rtol=1e-9, atol=1e-9)
+            np.testing.assert_allclose(s0[:base + 11], s1[:base + 11], rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_native_session_equals_device_step(pk, precision):
+    """vpb_smpc_session (one host call: staged block, captured graph of
+    sampler + fused step, host diagnostics) returns exactly the device step
+    on the same seed, follows a field rebuilt into a new buffer, and fills
+    e_pos / e_ori like the reference (vp/planner.py:620-629)."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.geometry import RigidTransform, quaternion_angle
+
+    chain, model = config.robot_7dof()
+    grid = mapping.VoxelGrid((-1.0, -1.0, 0.0), 0.05, (30, 30, 30))
+    occ = np.zeros((30, 30, 30), bool)
+    occ[12:16, 12:16, 10:14] = True
+    grid.set_log_odds(np.where(occ, 3.5, 0.0))
+    f1 = mapping.edt_3d(grid, outside_default=0.8)
+    occ[5:8, 20:24, 12:18] = True
+    grid.set_log_odds(np.where(occ, 3.5, 0.0))
+    f2 = mapping.edt_3d(grid, outside_default=0.8)
+    assert f1.sq_device.data_ptr() != f2.sq_device.data_ptr()
+    params = config.planner_params(7, {"samples": 700, "horizon": 24})
+    pl = planner.Planner(chain, model, params, precision)
+    state = robot.JointState(np.full(7, 0.1), np.linspace(-0.2, 0.2, 7), np.zeros(7))
+    goal = RigidTransform.from_vec7([0.3, -0.2, 0.7, 0.9, 0.1, 0.3, -0.2])
+    nom = 0.2 * np.cos(np.arange(24 * 7)).reshape(24, 7)
+    for field, seed in ((f1, 5), (f2, 6), (f1, 7)):
+        res = pl.smpc_step(state, goal, field, nom, seed)  # native session
+        eps = pl.sample_device(seed)
+        out = pl.smpc_step_device(state, goal, field, torch.from_numpy(nom).cuda(), eps).cpu().numpy()
+        ref = pl.unpack_step(out, state, goal, 24)
+        np.testing.assert_array_equal(res.command, ref.command)
+        np.testing.assert_array_equal(res.next_nominal, ref.next_nominal)
+        assert res.diagnostics.weighted_cost == ref.diagnostics.weighted_cost
+        assert res.diagnostics.best_cost == ref.diagnostics.best_cost
+        ee = robot.forward_kinematics(chain, state.q)[-1]
+        np.testing.assert_allclose(res.diagnostics.e_pos, np.linalg.norm(ee.translation - goal.translation),
+                                   rtol=1e-12)
+        np.testing.assert_allclose(res.diagnostics.e_ori, quaternion_angle(ee.rotation.to_quaternion(),
+                                                                           goal.rotation.to_quaternion()),
+                                   rtol=1e-9, atol=1e-12)
+    assert len(pl._sessions) == 1  # one session serves both field buffers
