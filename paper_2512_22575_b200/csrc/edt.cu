@@ -27,13 +27,15 @@ constexpr int32_t kNoSrc32 = INT_MAX;
 // Pass Z: bits -> u16 nearest-source distance along z.
 // One warp per (x, y) line of the box; lanes walk z in chunks of 32.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t load_bits_window(const uint32_t *__restrict__ w, int64_t z0) {
-  // 32 bits of the line starting at global z0 (z0 may be unaligned).
+__device__ __forceinline__ uint32_t load_bits_window(const uint32_t *__restrict__ w, int64_t z0,
+                                                     int64_t words_z = INT64_MAX) {
+  // 32 bits of the line starting at global z0 (z0 may be unaligned); bits
+  // past the line's last word read as 0.
   const int64_t wi = z0 >> 5;
   const int sh = (int)(z0 & 31);
-  const uint32_t a = __ldg(w + wi);
+  const uint32_t a = wi < words_z ? __ldg(w + wi) : 0u;
   if (sh == 0) return a;
-  const uint32_t b = __ldg(w + wi + 1);
+  const uint32_t b = wi + 1 < words_z ? __ldg(w + wi + 1) : 0u;
   return __funnelshift_r(a, b, sh);
 }
 
@@ -575,7 +577,7 @@ template <typename TOut>
 __device__ __forceinline__ void store_dist(TOut *p, int v);
 template <>
 __device__ __forceinline__ void store_dist<int32_t>(int32_t *p, int v) {
-  *p = v < 0 ? kNoSrc32 : v;
+  *p = v < 0 ? -1 : v;  // -1 = no source: the X pass copies it raw (== kTileInf)
 }
 template <>
 __device__ __forceinline__ void store_dist<float>(float *p, int v) {
@@ -635,59 +637,153 @@ __device__ void segmented_fh(uint32_t *tile, SegLine *segs, int len, int nlines_
   if (act && s == 0) merge_runs<WIDE>(tile, line, B, segs[line], 0, 1, 3);
   __syncthreads();
   if (!act || q0 >= q1) return;
-  const SegLine S = segs[line];
+  // segment bounds of the merged envelope in registers (indexed only through
+  // unrolled selects: no local memory)
+  int lo_[KSEG], hi_[KSEG];
+#pragma unroll
+  for (int t = 0; t < KSEG; ++t) {
+    lo_[t] = segs[line].lo[t];
+    hi_[t] = segs[line].hi[t];
+  }
+  auto sel = [&](const int (&a)[KSEG], int t) {
+    int v = a[0];
+#pragma unroll
+    for (int u = 1; u < KSEG; ++u) v = t == u ? a[u] : v;
+    return v;
+  };
   int total = 0;
 #pragma unroll
-  for (int t = 0; t < KSEG; ++t) total += S.hi[t] - S.lo[t];
+  for (int t = 0; t < KSEG; ++t) total += hi_[t] - lo_[t];
   TOut *dst = dst_base + line + (int64_t)q0 * stride;
   if (total == 0) {
     for (int q = q0; q < q1; ++q, dst += stride) store_dist<TOut>(dst, -1);
     return;
   }
-  // rank -> (segment, index)
-  auto at_rank = [&](int r, int &sg, int &ix) {
+  auto rank_to = [&](int r, int &sg, int &ix) {
+    sg = KSEG - 1;
+    ix = hi_[KSEG - 1] - 1;
+    bool found = false;
 #pragma unroll
     for (int t = 0; t < KSEG; ++t) {
-      const int sz = S.hi[t] - S.lo[t];
-      if (r < sz) {
+      const int sz = hi_[t] - lo_[t];
+      if (!found && r < sz) {
         sg = t;
-        ix = S.lo[t] + r;
-        return;
+        ix = lo_[t] + r;
+        found = true;
       }
-      r -= sz;
+      if (!found) r -= sz;
     }
-    sg = KSEG - 1;
-    ix = S.hi[KSEG - 1] - 1;
   };
+  auto elem = [&](int sg, int ix) { return elem_at(tile, line, B, sg, ix); };
   // largest r with r == 0 or s(e_{r-1}, e_r) < q0
   int lo = 0, hi = total - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
     int sa, ia, sb, ib;
-    at_rank(mid - 1, sa, ia);
-    at_rank(mid, sb, ib);
-    if (boundary_lt<WIDE>(elem_at(tile, line, B, sa, ia), elem_at(tile, line, B, sb, ib), q0))
+    rank_to(mid - 1, sa, ia);
+    rank_to(mid, sb, ib);
+    if (boundary_lt<WIDE>(elem(sa, ia), elem(sb, ib), q0))
       lo = mid;
     else
       hi = mid - 1;
   }
   int cs, ci;
-  at_rank(lo, cs, ci);
-  Elem cur = elem_at(tile, line, B, cs, ci);
-  int ns = -1, ni = 0;
-  Elem nxt{0, 0, 0};
-  bool has_next = next_elem(S, cs, ci, KSEG - 1, ns, ni);
-  if (has_next) nxt = elem_at(tile, line, B, ns, ni);
-  for (int q = q0; q < q1; ++q, dst += stride) {
-    while (has_next && boundary_lt<WIDE>(cur, nxt, q)) {
-      cur = nxt;
-      cs = ns;
-      ci = ni;
-      has_next = next_elem(S, cs, ci, KSEG - 1, ns, ni);
-      if (has_next) nxt = elem_at(tile, line, B, ns, ni);
+  rank_to(lo, cs, ci);
+  int rk = lo;  // rank of cur
+  Elem cur = elem(cs, ci);
+  // next element: same segment, else the next non-empty one
+  auto step = [&](int &sg, int &ix) {
+    if (ix + 1 < sel(hi_, sg)) {
+      ++ix;
+      return;
     }
-    const int d = q - cur.v;
-    store_dist<TOut>(dst, d * d + cur.f);
+    int ns = sg, ni = ix;
+#pragma unroll
+    for (int t = KSEG - 1; t >= 1; --t)
+      if (t > sg && hi_[t] > lo_[t]) {
+        ns = t;
+        ni = lo_[t];
+      }
+    sg = ns;
+    ix = ni;
+  };
+  int ns = cs, ni = ci;
+  bool has_next = rk + 1 < total;
+  Elem nxt = cur;
+  if (has_next) {
+    step(ns, ni);
+    nxt = elem(ns, ni);
+  }
+  // The envelope changes to `nxt` at the first q with F_n - F_c < 2 q (v_n - v_c)
+  // (v_n > v_c): q_sw = floor((F_n - F_c) / (2 (v_n - v_c))) + 1.  Between
+  // switches the outputs are a run of (q - v)^2 + f.
+  auto q_switch = [&](const Elem &c, const Elem &nx) -> int {
+    const long long num = (long long)nx.F - c.F, den = 2ll * (nx.v - c.v);
+    long long fl = num / den;
+    if ((num % den != 0) && (num < 0)) --fl;  // floor for a negative numerator
+    return (int)(fl + 1);
+  };
+  int qs = has_next ? q_switch(cur, nxt) : 0x7fffffff;
+  int q = q0;
+  while (q < q1) {
+    while (q >= qs) {  // advance (possibly over several parabolas)
+      cur = nxt;
+      ++rk;
+      has_next = rk + 1 < total;
+      if (has_next) {
+        step(ns, ni);
+        nxt = elem(ns, ni);
+        qs = q_switch(cur, nxt);
+      } else {
+        qs = 0x7fffffff;
+      }
+    }
+    const int qe = qs < q1 ? qs : q1;
+    const int v = cur.v, f = cur.f;
+    for (; q < qe; ++q, dst += stride) {
+      const int d = q - v;
+      store_dist<TOut>(dst, d * d + f);
+    }
+  }
+}
+
+// Per (x, y) line of the box, per 32-z word w of the box line: the nearest
+// source strictly left of the word (box-local z + 1, 0 = none) in the low 16
+// bits and the nearest strictly right (0xFFFF = none) in the high 16 bits.
+// One thread per line; 2 MB of bits in, n0 n1 ceil(n2 / 32) words out.
+__global__ void __launch_bounds__(256) edt_line_lr_kernel(const uint32_t *__restrict__ bits, int64_t gy,
+                                                          int64_t words_z, int64_t lo0, int64_t lo1, int lo2,
+                                                          int n0, int n1, int n2, uint32_t *__restrict__ lr) {
+  const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (line >= (int64_t)n0 * n1) return;
+  const int64_t i0 = line / n1, i1 = line - i0 * n1;
+  const uint32_t *w = bits + ((lo0 + i0) * gy + (lo1 + i1)) * words_z;
+  const int nw = (n2 + 31) >> 5;
+  uint32_t *o = lr + line * nw;
+  // all of the line's words in flight at once (nw <= 32 on this path)
+  uint32_t m[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    uint32_t v = 0u;
+    if (c < nw) {
+      v = load_bits_window(w, lo2 + 32 * c, words_z);
+      const int valid = n2 - 32 * c;
+      if (valid < 32) v &= (1u << valid) - 1u;
+    }
+    m[c] = v;
+  }
+  uint32_t left[32];
+  int last = -1;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    left[c] = (uint32_t)(last + 1);
+    if (m[c]) last = 32 * c + 31 - __clz(m[c]);
+  }
+  int first = 0xFFFF;
+#pragma unroll
+  for (int c = 31; c >= 0; --c) {
+    if (c < nw) o[c] = left[c] | ((uint32_t)first << 16);
+    if (m[c]) first = 32 * c + __ffs(m[c]) - 1;
   }
 }
 
@@ -700,7 +796,8 @@ __device__ void segmented_fh(uint32_t *tile, SegLine *segs, int len, int nlines_
 template <bool WIDE>
 __global__ void __launch_bounds__(ETHREADS) edt_zy_kernel(const uint32_t *__restrict__ bits, int64_t gy,
                                                           int64_t words_z, int64_t lo0, int64_t lo1, int lo2,
-                                                          int n1, int n2, int32_t *__restrict__ out) {
+                                                          int n1, int n2, const uint32_t *__restrict__ lr,
+                                                          int32_t *__restrict__ out) {
   extern __shared__ uint32_t smem[];
   uint32_t *tile = smem;                                                // [n1][32]
   SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)n1 * 32);  // [32]
@@ -711,40 +808,39 @@ __global__ void __launch_bounds__(ETHREADS) edt_zy_kernel(const uint32_t *__rest
   const int nlines = min(32, n2 - zc * 32);
   const uint32_t le_mask = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
   const uint32_t ge_mask = 0xffffffffu << lane;
-  const uint32_t below_zc = zc == 0 ? 0u : (0xffffffffu >> (32 - zc));         // words < zc
-  const uint32_t above_zc = zc >= 31 ? 0u : (0xffffffffu << (zc + 1));          // words > zc
   const int B = (n1 + KSEG - 1) / KSEG;
-  const int zb_lane = lo2 + 32 * lane;
-  const int wi_lane = zb_lane >> 5, sh_lane = zb_lane & 31;
-  const int valid_lane = n2 - 32 * lane;
+  const int z = 32 * zc + lane;
+  const int valid = n2 - 32 * zc;
+  const uint32_t vmask = valid < 32 ? (1u << valid) - 1u : 0xffffffffu;
   const uint32_t *wbase = bits + ((lo0 + x) * gy + lo1) * words_z;
-  // warp w fills the rows of segment w (its rotated column is warp-uniform)
+  const uint32_t *lrbase = lr + (x * n1) * (int64_t)nw + zc;
+  uint32_t *dcol = tile + ((lane + 8 * warp) & 31);
+  // warp w fills the rows of segment w (its rotated column is warp-uniform):
+  // per row one broadcast word + one broadcast (left, right) pair
   const int y0 = warp * B, y1 = min(n1, y0 + B);
-  for (int y = y0; y < y1; ++y) {
-    const uint32_t *w = wbase + (int64_t)y * words_z;
-    uint32_t word = 0;
-    if (lane < nw) {
-      const uint32_t a = __ldg(w + wi_lane);
-      const uint32_t b = (sh_lane != 0 && wi_lane + 1 < words_z) ? __ldg(w + wi_lane + 1) : 0u;
-      word = sh_lane ? __funnelshift_r(a, b, sh_lane) : a;
-      if (valid_lane < 32) word &= (1u << valid_lane) - 1u;
-    }
-    const uint32_t nz = __ballot_sync(kFull, word != 0u);
-    const uint32_t wc = __shfl_sync(kFull, word, zc);
-    const uint32_t lmask = nz & below_zc, rmask = nz & above_zc;
-    const int lw = lmask ? 31 - __clz(lmask) : 0;
-    const int rw = rmask ? __ffs(rmask) - 1 : 0;
-    const uint32_t lword = __shfl_sync(kFull, word, lw);
-    const uint32_t rword = __shfl_sync(kFull, word, rw);
-    const int z = 32 * zc + lane;
-    const uint32_t le = wc & le_mask, ge = wc & ge_mask;
-    const int left = le ? 32 * zc + 31 - __clz(le) : (lmask ? 32 * lw + 31 - __clz(lword) : -1);
-    const int right = ge ? 32 * zc + __ffs(ge) - 1 : (rmask ? 32 * rw + __ffs(rword) - 1 : 0x7fffffff);
+  auto fill = [&](int y, uint32_t word, uint32_t lrv) {
+    word &= vmask;
+    const uint32_t le = word & le_mask, ge = word & ge_mask;
+    const int left = le ? 32 * zc + 31 - __clz(le) : (int)(lrv & 0xFFFFu) - 1;
+    const int rgt = ge ? 32 * zc + __ffs(ge) - 1 : (int)(lrv >> 16);
     int d = 0x7fffffff;
     if (left >= 0) d = z - left;
-    if (right != 0x7fffffff) d = min(d, right - z);
-    tile[y * 32 + ((lane + 8 * warp) & 31)] = (lane < nlines && d != 0x7fffffff) ? (uint32_t)(d * d) : kTileInf;
+    if (rgt != 0xFFFF) d = min(d, rgt - z);
+    dcol[y * 32] = (lane < nlines && d != 0x7fffffff) ? (uint32_t)(d * d) : kTileInf;
+  };
+  int y = y0;
+  for (; y + 4 <= y1; y += 4) {
+    uint32_t wd[4], lv[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      wd[t] = load_bits_window(wbase + (int64_t)(y + t) * words_z, lo2 + 32 * zc, words_z);
+      lv[t] = __ldg(lrbase + (int64_t)(y + t) * nw);
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) fill(y + t, wd[t], lv[t]);
   }
+  for (; y < y1; ++y)
+    fill(y, load_bits_window(wbase + (int64_t)y * words_z, lo2 + 32 * zc, words_z), __ldg(lrbase + (int64_t)y * nw));
   __syncthreads();
   int32_t *dst = out + (x * n1) * (int64_t)n2 + zc * 32;
   segmented_fh<int32_t, WIDE>(tile, segs, n1, nlines, dst, n2);
@@ -765,22 +861,25 @@ __global__ void __launch_bounds__(ETHREADS) edt_x_kernel(const int32_t *__restri
   const int B = (n0 + KSEG - 1) / KSEG;
   const int64_t row_stride = (int64_t)n1 * n2;
   const bool on = lane < nlines;
-  // warp w fills segment w's rows (so the rotated column is warp-uniform)
-  const int r0 = warp * B, r1 = min(n0, r0 + B);
-  const int32_t *src = g + y * n2 + zc * 32 + lane + (int64_t)r0 * row_stride;
-  uint32_t *dcol = tile + ((lane + 8 * warp) & 31);
-  int r = r0;
-  for (; r + 4 <= r1; r += 4, src += 4 * row_stride) {
-    int32_t v[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) v[t] = on ? __ldg(src + t * row_stride) : kNoSrc32;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) dcol[(r + t) * 32] = v[t] == kNoSrc32 ? kTileInf : (uint32_t)v[t];
+  // Stage the [n0][32] tile with asynchronous 16-byte copies (all rows in
+  // flight at once; g holds -1 = kTileInf for "no source", so the copy is
+  // raw).  Row x lands rotated by 8 * (segment of x) words, the column
+  // layout segmented_fh expects.  Lanes past the line end are zero-filled
+  // (inactive in the envelope).
+  (void)on;
+  const int32_t *gbase = g + y * n2 + zc * 32;
+  const int bytes_row = nlines * 4;
+  for (int i = tid; i < n0 * 8; i += ETHREADS) {
+    const int r = i >> 3, piece = i & 7;  // 8 x 16 B per 128 B row
+    const int sgm = r / B;
+    const int col = (piece * 4 + 8 * sgm) & 31;
+    const int rem = bytes_row - piece * 16;
+    const int nb = rem >= 16 ? 16 : (rem > 0 ? rem : 0);
+    const int32_t *src = nb > 0 ? gbase + (int64_t)r * row_stride + piece * 4 : g;
+    const unsigned dst_s = (unsigned)__cvta_generic_to_shared(tile + r * 32 + col);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_s), "l"(src), "r"(nb) : "memory");
   }
-  for (; r < r1; ++r, src += row_stride) {
-    const int32_t v = on ? __ldg(src) : kNoSrc32;
-    dcol[r * 32] = v == kNoSrc32 ? kTileInf : (uint32_t)v;
-  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
   float *dst = out + y * n2 + zc * 32;
   segmented_fh<float, WIDE>(tile, segs, n0, nlines, dst, row_stride);
@@ -815,7 +914,10 @@ extern "C" {
 
 size_t vpb_edt3d_workspace_bytes(const int64_t n[3]) {
   const size_t vox = (size_t)n[0] * (size_t)n[1] * (size_t)n[2];
-  return align_up(vox * sizeof(uint16_t), 256) + align_up(vox * sizeof(int32_t), 256);
+  // u16 z distances or the per-word left/right table (n0 n1 ceil(n2/32) u32), then int32 g
+  const size_t lrb = (size_t)n[0] * (size_t)n[1] * (size_t)((n[2] + 31) / 32) * 4;
+  return align_up(vox * sizeof(uint16_t) > lrb ? vox * sizeof(uint16_t) : lrb, 256) +
+         align_up(vox * sizeof(int32_t), 256);
 }
 
 int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], double thr, int use_bits,
@@ -830,11 +932,12 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], dou
   cudaStream_t s = as_stream(stream);
   const size_t vox = (size_t)n[0] * (size_t)n[1] * (size_t)n[2];
   uint16_t *dz = reinterpret_cast<uint16_t *>(workspace);
-  int32_t *g2 = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(workspace) + align_up(vox * 2, 256));
+  const size_t lrb = (size_t)n[0] * (size_t)n[1] * (size_t)((n[2] + 31) / 32) * 4;
+  int32_t *g2 = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(workspace) + align_up(vox * 2 > lrb ? vox * 2 : lrb, 256));
   const int64_t lines_z = n[0] * n[1];
   const int64_t maxd = n[0] > n[1] ? (n[0] > n[2] ? n[0] : n[2]) : (n[1] > n[2] ? n[1] : n[2]);
   int rc;
-  if (maxd <= 1024 && use_bits && n[0] <= 65535 && n[1] <= 65535) {
+  if (maxd <= 1024 && use_bits && n[0] <= 65535 && n[1] <= 65535 && n[2] % 4 == 0) {  // 16 B-aligned g rows
     VPB_REQUIRE(grid->occ_bits, "use_bits set but grid->occ_bits is null");
     // Pass Z+Y fused from the occupancy words, then pass X.
     const size_t smem_zy = (size_t)n[1] * 32 * 4 + sizeof(SegLine) * 32;
@@ -845,8 +948,16 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], dou
     if (smem_zy > 48 * 1024) VPB_CUDA(cudaFuncSetAttribute(kzy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
     if (smem_x > 48 * 1024) VPB_CUDA(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
     const unsigned zch = (unsigned)((n[2] + 31) / 32);
+    // per-line left/right source table (fits the u16 z-distance slot of the workspace)
+    uint32_t *lr = reinterpret_cast<uint32_t *>(workspace);
+    const int64_t lines = n[0] * n[1];
+    edt_line_lr_kernel<<<(unsigned)ceil_div(lines, 256), 256, 0, s>>>(
+        grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], (int)lo[2], (int)n[0], (int)n[1],
+        (int)n[2], lr);
+    rc = check_launch("edt_line_lr_kernel");
+    if (rc) return rc;
     kzy<<<dim3(zch, (unsigned)n[0]), ETHREADS, smem_zy, s>>>(grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32),
-                                                             lo[0], lo[1], (int)lo[2], (int)n[1], (int)n[2], g2);
+                                                             lo[0], lo[1], (int)lo[2], (int)n[1], (int)n[2], lr, g2);
     rc = check_launch("edt_zy_kernel");
     if (rc) return rc;
     kx<<<dim3(zch, (unsigned)n[1]), ETHREADS, smem_x, s>>>(g2, (int)n[0], (int)n[1], (int)n[2], out_sq);
