@@ -52,10 +52,13 @@ class Workspace:
     _bufs: dict = {}
 
     @classmethod
-    def get(cls, dev: torch.device, tag: str, nbytes: int) -> torch.Tensor:
+    def get(cls, dev: torch.device, tag: str, nbytes: int, zeroed: bool = False) -> torch.Tensor:
+        """``zeroed``: zero-filled when (re)allocated (buffers holding counters
+        that the kernels return to zero themselves)."""
         key = (str(dev), tag)
         buf = cls._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+            alloc = torch.zeros if zeroed else torch.empty
+            buf = alloc(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
             cls._bufs[key] = buf
         return buf

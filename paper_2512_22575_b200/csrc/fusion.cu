@@ -13,6 +13,8 @@
 // observed accesses are coalesced and the occupancy word is rebuilt with one
 // ballot.  Voxels outside the robot's bounding box skip the sphere test;
 // voxels whose projection misses the image touch no memory at all.
+#include <climits>
+
 #include "vpb_common.cuh"
 
 namespace vpb {
@@ -132,42 +134,42 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
     bb_v0 = __ldg(A.bbox + 2);
     bb_v1 = __ldg(A.bbox + 3);
   }
+  // ---- range early-out (warp-uniform): the voxel centres of z in [za, zb]
+  // lie on a segment whose image is the segment between its endpoints'
+  // projections (qz > 0 at both ends => along it).  If that pixel range,
+  // widened by the error bound, misses every usable pixel, every voxel of the
+  // range is a reference "skip" -- unless the range may touch a mask sphere.
+  auto range_skip = [&](int64_t za, int64_t zb) -> bool {
+    const float pza = A.of2 + ((float)za + 0.5f) * A.voxf, pzb = A.of2 + ((float)zb + 0.5f) * A.voxf;
+    const bool maybe_mask = line_mask && !(pzb < A.bb_lo[2] || pza > A.bb_hi[2]);
+    if (maybe_mask) return false;
+    const float qza = fmaf(A.rf[8], pza, qz0), qzb = fmaf(A.rf[8], pzb, qz0);
+    if (qza < -dq && qzb < -dq) return true;  // whole range behind the camera
+    if (!(qza > 2.0f * dq && qzb > 2.0f * dq)) return false;
+    const float ia = __fdividef(1.0f, qza), ib = __fdividef(1.0f, qzb);
+    const float qxa = fmaf(A.rf[2], pza, qx0), qxb = fmaf(A.rf[2], pzb, qx0);
+    const float qya = fmaf(A.rf[5], pza, qy0), qyb = fmaf(A.rf[5], pzb, qy0);
+    const float ua = fmaf(A.fxf * qxa, ia, A.cxh), ub = fmaf(A.fxf * qxb, ib, A.cxh);
+    const float va = fmaf(A.fyf * qya, ia, A.cyh), vb = fmaf(A.fyf * qyb, ib, A.cyh);
+    const float ima = fmaxf(ia, ib);
+    const float du = A.ku * dq * (fmaxf(fabsf(qxa), fabsf(qxb)) + fmaxf(qza, qzb) + dq) * ima * ima +
+                     1e-6f * fmaxf(fabsf(ua), fabsf(ub)) + A.au;
+    const float dv = A.kv * dq * (fmaxf(fabsf(qya), fabsf(qyb)) + fmaxf(qza, qzb) + dq) * ima * ima +
+                     1e-6f * fmaxf(fabsf(va), fabsf(vb)) + A.av;
+    const float u_lo = fminf(ua, ub) - du - 1.0f, u_hi = fmaxf(ua, ub) + du + 1.0f;
+    const float v_lo = fminf(va, vb) - dv - 1.0f, v_hi = fmaxf(va, vb) + dv + 1.0f;
+    return bb_u1 < bb_u0 || u_hi < (float)bb_u0 || u_lo > (float)(bb_u1 + 1) || v_hi < (float)bb_v0 ||
+           v_lo > (float)(bb_v1 + 1);
+  };
+  // whole line first: most lines of a large box never meet a usable pixel
+  if (A.bbox && range_skip(A.lo2, A.lo2 + A.n2 - 1)) return;
   for (int64_t wz = A.wz_begin; wz < A.wz_begin + A.wz_count; ++wz) {
     const int64_t z = wz * 32 + lane;
     const bool in_box = (z >= A.lo2) && (z < A.lo2 + A.n2);
-    // ---- chunk early-out (warp-uniform): the 32 voxel centres lie on a
-    // segment whose image is the segment between its endpoints' projections
-    // (qz > 0 at both ends => along it).  If that pixel range, widened by the
-    // error bound, misses every usable pixel, every voxel of the chunk is a
-    // reference "skip" -- unless the chunk may touch a mask sphere.
     if (A.bbox) {
       const int64_t za = wz * 32 > A.lo2 ? wz * 32 : A.lo2;
       const int64_t zb = (wz * 32 + 31) < (A.lo2 + A.n2 - 1) ? (wz * 32 + 31) : (A.lo2 + A.n2 - 1);
-      const float pza = A.of2 + ((float)za + 0.5f) * A.voxf, pzb = A.of2 + ((float)zb + 0.5f) * A.voxf;
-      const bool maybe_mask = line_mask && !(pzb < A.bb_lo[2] || pza > A.bb_hi[2]);
-      const float qza = fmaf(A.rf[8], pza, qz0), qzb = fmaf(A.rf[8], pzb, qz0);
-      bool skip = false;
-      if (!maybe_mask) {
-        if (qza < -dq && qzb < -dq) {
-          skip = true;  // whole chunk behind the camera
-        } else if (qza > 2.0f * dq && qzb > 2.0f * dq) {
-          const float ia = __fdividef(1.0f, qza), ib = __fdividef(1.0f, qzb);
-          const float qxa = fmaf(A.rf[2], pza, qx0), qxb = fmaf(A.rf[2], pzb, qx0);
-          const float qya = fmaf(A.rf[5], pza, qy0), qyb = fmaf(A.rf[5], pzb, qy0);
-          const float ua = fmaf(A.fxf * qxa, ia, A.cxh), ub = fmaf(A.fxf * qxb, ib, A.cxh);
-          const float va = fmaf(A.fyf * qya, ia, A.cyh), vb = fmaf(A.fyf * qyb, ib, A.cyh);
-          const float ima = fmaxf(ia, ib);
-          const float du = A.ku * dq * (fmaxf(fabsf(qxa), fabsf(qxb)) + fmaxf(qza, qzb) + dq) * ima * ima +
-                           1e-6f * fmaxf(fabsf(ua), fabsf(ub)) + A.au;
-          const float dv = A.kv * dq * (fmaxf(fabsf(qya), fabsf(qyb)) + fmaxf(qza, qzb) + dq) * ima * ima +
-                           1e-6f * fmaxf(fabsf(va), fabsf(vb)) + A.av;
-          const float u_lo = fminf(ua, ub) - du - 1.0f, u_hi = fmaxf(ua, ub) + du + 1.0f;
-          const float v_lo = fminf(va, vb) - dv - 1.0f, v_hi = fmaxf(va, vb) + dv + 1.0f;
-          skip = bb_u1 < bb_u0 || u_hi < (float)bb_u0 || u_lo > (float)(bb_u1 + 1) || v_hi < (float)bb_v0 ||
-                 v_lo > (float)(bb_v1 + 1);
-        }
-      }
-      if (skip) continue;
+      if (range_skip(za, zb)) continue;
     }
     bool exact = false;
     int fast = 0;  // 1 = certain hit, 2 = certain miss (fp32 classification)
@@ -260,7 +262,9 @@ struct MaskPixArgs {
   double r[9], t[3];
   int n_mask;
   int encode_usable;  // out = 1 masked, 2 usable return, 0 otherwise
-  int *bbox;          // optional: [umin, umax, vmin, vmax] of usable pixels (atomics)
+  int *bbox;          // optional: [umin, umax, vmin, vmax] of usable pixels
+  int *partials;      // per-CTA rectangles (bbox != null)
+  unsigned *counter;  // CTA ticket, zero between launches (the last CTA resets it)
   double pad;
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr[VPB_MAX_MASK_SPHERES];
@@ -268,10 +272,11 @@ struct MaskPixArgs {
 
 // vp/mapping.py:357-380, one thread per pixel.
 __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constant__ MaskPixArgs A) {
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= A.width * A.height) return;
+  const int64_t idx0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool px = idx0 < A.width * A.height;  // (threads past the image join the CTA reduction)
+  const int64_t idx = px ? idx0 : 0;
   const int64_t vv = idx / A.width, uu = idx - vv * A.width;
-  const double d = A.depth[idx];
+  const double d = px ? A.depth[idx] : -1.0;
   uint8_t inside = 0;
   const bool valid = d >= A.d_min && d <= A.d_max;
   if (A.n_mask > 0 && valid) {
@@ -290,13 +295,59 @@ __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constan
       if (dadd(dadd(dmul(dx, dx), dmul(dy, dy)), dmul(dz, dz)) < dmul(r, r)) inside = 1;
     }
   }
-  const uint8_t code = inside ? 1 : (valid ? 2 : 0);
-  A.out[idx] = A.encode_usable ? code : inside;
-  if (A.bbox && code == 2) {
-    atomicMin(A.bbox + 0, (int)uu);
-    atomicMax(A.bbox + 1, (int)uu);
-    atomicMin(A.bbox + 2, (int)vv);
-    atomicMax(A.bbox + 3, (int)vv);
+  const uint8_t code = px ? (inside ? 1 : (valid ? 2 : 0)) : 0;
+  if (px) A.out[idx] = A.encode_usable ? code : inside;
+  if (A.bbox) {
+    // rectangle of the usable pixels: CTA reduction, then the last CTA
+    // (ticket) reduces the CTA rectangles -- no atomics on the rectangle and
+    // no memset before the launch
+    __shared__ int red[4][8];
+    __shared__ unsigned last;
+    const bool use = code == 2;
+    int r0 = __reduce_min_sync(kFull, use ? (int)uu : INT_MAX);
+    int r1 = __reduce_max_sync(kFull, use ? (int)uu : INT_MIN);
+    int r2 = __reduce_min_sync(kFull, use ? (int)vv : INT_MAX);
+    int r3 = __reduce_max_sync(kFull, use ? (int)vv : INT_MIN);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) {
+      red[0][warp] = r0;
+      red[1][warp] = r1;
+      red[2][warp] = r2;
+      red[3][warp] = r3;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+        r0 = min(r0, red[0][w]);
+        r1 = max(r1, red[1][w]);
+        r2 = min(r2, red[2][w]);
+        r3 = max(r3, red[3][w]);
+      }
+      int *pp = A.partials + 4 * blockIdx.x;
+      pp[0] = r0, pp[1] = r1, pp[2] = r2, pp[3] = r3;
+      __threadfence();
+      last = atomicAdd(A.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (last && threadIdx.x < 32) {
+      __threadfence();
+      int m0 = INT_MAX, m1 = INT_MIN, m2 = INT_MAX, m3 = INT_MIN;
+      for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
+        const int *pp = A.partials + 4 * b;
+        m0 = min(m0, __ldcg(pp + 0));
+        m1 = max(m1, __ldcg(pp + 1));
+        m2 = min(m2, __ldcg(pp + 2));
+        m3 = max(m3, __ldcg(pp + 3));
+      }
+      m0 = __reduce_min_sync(kFull, m0);
+      m1 = __reduce_max_sync(kFull, m1);
+      m2 = __reduce_min_sync(kFull, m2);
+      m3 = __reduce_max_sync(kFull, m3);
+      if (threadIdx.x == 0) {
+        A.bbox[0] = m0, A.bbox[1] = m1, A.bbox[2] = m2, A.bbox[3] = m3;
+        *A.counter = 0u;
+      }
+    }
   }
 }
 
@@ -374,6 +425,10 @@ static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const 
   A.n_mask = (int)n_mask;
   A.encode_usable = encode;
   A.bbox = bbox;
+  if (bbox) {  // scratch after the rectangle: [ticket, pad..., CTA rectangles]
+    A.counter = reinterpret_cast<unsigned *>(bbox + 4);
+    A.partials = bbox + 8;
+  }
   A.pad = pad;
   const int64_t npx = cam->width * cam->height;
   if (npx == 0) return VPB_OK;
@@ -464,6 +519,11 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3
   return fuse_impl(grid, lo, n, cam, depth, pixel_masked, centers, radii, n_mask, p, 0, nullptr, stream);
 }
 
+int64_t vpb_pixel_scratch_bytes(int64_t width, int64_t height) {
+  const int64_t npx = width * height;
+  return (int64_t)align_up((size_t)npx, 16) + 32 + 16 * ceil_div(npx > 0 ? npx : 1, 256) + 64;
+}
+
 int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
                          const double *depth, const double *centers, const double *radii, int64_t n_mask,
                          double mask_pad, const vpb_map_params *params, uint8_t *pixel_scratch, void *stream) {
@@ -472,9 +532,6 @@ int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3], const int64_
   // return; followed by the bounding rectangle of the usable pixels
   const int64_t npx = cam->width * cam->height;
   int *bbox = reinterpret_cast<int *>(pixel_scratch + align_up((size_t)npx, 16));
-  VPB_CUDA(cudaMemsetAsync(bbox, 0x7F, 16, as_stream(stream)));
-  VPB_CUDA(cudaMemsetAsync(bbox + 1, 0x80, 4, as_stream(stream)));
-  VPB_CUDA(cudaMemsetAsync(bbox + 3, 0x80, 4, as_stream(stream)));
   int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, bbox, stream);
   if (rc) return rc;
   return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, bbox, stream);

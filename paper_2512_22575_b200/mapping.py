@@ -311,7 +311,8 @@ def update_occupancy(grid: VoxelGrid, depth: DepthImage, cam: CameraModel, mask=
     centers, radii = _mask_arrays(mask)
     dev = grid.device
     d_dev = depth.device_tensor(dev)
-    scratch = D.Workspace.get(dev, "pixel_mask", cam.width * cam.height + 64)
+    scratch = D.Workspace.get(dev, "pixel_mask", int(load().vpb_pixel_scratch_bytes(cam.width, cam.height)),
+                              zeroed=True)
     check(load().vpb_update_occupancy(
         grid._struct(), i64x3(box.lo), i64x3(box.shape), cam._struct(), D.ptr(d_dev),
         D.host_ptr(centers), D.host_ptr(radii), centers.shape[0], float(mask_pad),
