@@ -245,6 +245,18 @@ int vpb_smpc_step(const vpb_problem *prob, const vpb_field *field,
                   int precision, double *costs, uint8_t *flags, double *out,
                   void *workspace, size_t workspace_bytes, void *stream);
 
+/* Draw + step in one call: the perturbations of vpb_sample_perturbations
+ * (same seed / m_offset / window / sigma -> identical values) go to eps_out
+ * (dev, M x H x n, f32 for VPB_PREC_F32, f64 otherwise) and the step runs on
+ * them -- the single-device step into `out` or this shard's partial into
+ * `part_out` (exactly one non-NULL).  For the compiled robot topology in fp32
+ * with window <= 5 the draws happen inside the step kernel (no sampler
+ * launch, no read-back of the noise). */
+int vpb_smpc_generate(const vpb_problem *prob, const vpb_field *field, uint64_t seed, const uint64_t *seed_dev,
+                      int64_t m_offset, int64_t window, const double *sigma, const double *nominal, int64_t M,
+                      int precision, double *costs, uint8_t *flags, void *eps_out, double *part_out, double *out,
+                      void *workspace, size_t workspace_bytes, void *stream);
+
 /* Multi-device finish: merge R rank partials (R x partial_len, dev) in rank
  * order and run the same tail as vpb_smpc_step into `out`. */
 size_t vpb_smpc_finish_workspace_bytes(int64_t n_parts, int64_t H, int64_t n);

@@ -107,6 +107,8 @@ SIGNATURES = {
     "vpb_smpc_out_len": (_i64, [_i64, _i64]),
     "vpb_smpc_step": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _p, ctypes.c_int, _p, _i64, ctypes.c_int, _p,
                                      _p, _p, _p, _sz, _p]),
+    "vpb_smpc_generate": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), ctypes.c_uint64, _p, _i64, _i64, _p, _p, _i64,
+                                         ctypes.c_int, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "vpb_smpc_finish_workspace_bytes": (_sz, [_i64, _i64, _i64]),
     "vpb_smpc_finish": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _p, _i64, _p, ctypes.c_int, _p, _p,
                                        _sz, _p]),

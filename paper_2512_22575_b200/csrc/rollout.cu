@@ -27,6 +27,7 @@
 #include <cfloat>
 #include <cstdlib>
 
+#include "noise.cuh"
 #include "rollout_fixed.cuh"
 
 namespace vpb {
@@ -428,7 +429,9 @@ constexpr int smpc_min_blocks() {
 template <typename T, typename ET, typename Topo>
 __device__ __forceinline__ void fixed_candidate(const Prob<T> &P, const Dyn<T> &D, const ET *ctrl,
                                                 const double *nominal, bool valid, int H, int shift, int sub,
-                                                int nsub, double *sums_slot, double *term_slot, int *fail_slot) {
+                                                int nsub, double *sums_slot, double *term_slot, int *fail_slot,
+                                                const NoiseGen *gen = nullptr, int64_t m_loc = 0,
+                                                float *eps_out = nullptr) {
   constexpr int NJ = Topo::NJ;
   const int lane = threadIdx.x & 31;
   const Split W = make_split<Topo>(sub, nsub);
@@ -447,11 +450,20 @@ __device__ __forceinline__ void fixed_candidate(const Prob<T> &P, const Dyn<T> &
     const bool act = valid && k < H;
     T qe[NJ];
     T lim = 0, sm = 0, nu = 0;
+    float gz[NJ];  // on-the-fly perturbation (noise.cuh), warp-uniform branch
+    if (gen) {
+      candidate_noise<NJ, 2>(*gen, m_loc, H, ch, lane, gz);
+      if (act && eps_out) {
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) eps_out[((size_t)m_loc * H + k) * NJ + j] = gz[j];
+      }
+    }
 #pragma unroll
     for (int j = 0; j < NJ; ++j) {
       double v = 0.0;
       if (act) {
-        if (ctrl) v = load_e<ET>(ctrl + (size_t)k * NJ + j);
+        if (gen) v = (double)gz[j];
+        else if (ctrl) v = load_e<ET>(ctrl + (size_t)k * NJ + j);
         if (nominal) v += nominal[(size_t)k * NJ + j];
       }
       const T uj = (T)v;
@@ -786,6 +798,9 @@ struct SmpcIO {
   unsigned long long *trace;  // optional per-phase %globaltimer stamps (tools/smpc_trace.py)
   double *pro;  // [NWF][4] q_0 terms per split warp (fixed path, prologue block 0)
   double *cand_costs;  // [M] candidate costs when io.costs is null (workspace)
+  NoiseGen gen;    // on-the-fly perturbations (fixed path) when gen_on
+  int gen_on;
+  float *eps_out;  // where the drawn perturbations go (== eps for the merge)
 };
 
 // U* = nominal + N / Z, the clipped command and the shifted warm start
@@ -1111,9 +1126,10 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
       const bool cand = state == 1;
       const ET *ctrl = (cand && m < io.M) ? eps + (size_t)m * hn : nullptr;
       const double *nom = state == 1 ? io.nominal : (state == 2 ? io.out : nullptr);
-      fixed_candidate<T, ET, Topo>(P, D, ctrl, nom, cand ? m < io.M : true, state == 0 ? 1 : P.H,
-                                   state == 0 ? 0 : 1, cand ? 0 : warp, cand ? 1 : NWF, S.sums + warp * 6,
-                                   S.cost + warp, S.fail + warp);
+      fixed_candidate<T, ET, Topo>(P, D, io.gen_on ? nullptr : ctrl, nom, cand ? m < io.M : true,
+                                   state == 0 ? 1 : P.H, state == 0 ? 0 : 1, cand ? 0 : warp, cand ? 1 : NWF,
+                                   S.sums + warp * 6, S.cost + warp, S.fail + warp,
+                                   (cand && io.gen_on) ? &io.gen : nullptr, m, io.eps_out);
       __syncthreads();
       if (state == 0) {
         if (threadIdx.x < NWF) {
@@ -1622,7 +1638,7 @@ int64_t vpb_smpc_out_len(int64_t H, int64_t n) { return 2 * H * n + n + 13; }
 static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const void *eps, int dtype,
                        const double *nominal, int64_t M, int64_t m_offset, int precision, double *costs,
                        uint8_t *flags, double *part_out, double *out, void *workspace, size_t workspace_bytes,
-                       cudaStream_t s) {
+                       cudaStream_t s, const NoiseGen *gen = nullptr) {
   int rc = prob_checks(prob, precision, dtype);
   if (rc) return rc;
   VPB_REQUIRE(eps && nominal && M >= 1, "bad arguments to the SMPC step");
@@ -1655,6 +1671,11 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   io.dyn = prob->dyn_state;
   io.trace = g_smpc_trace;
   const int topo = fixed_topology_disabled() ? 0 : topo_id(prob);
+  if (gen) {  // fused draw (eps is the output buffer of the draws)
+    io.gen = *gen;
+    io.gen_on = 1;
+    io.eps_out = reinterpret_cast<float *>(const_cast<void *>(eps));
+  }
   if (precision == VPB_PREC_F64) {
     Prob<double> P;
     if ((rc = build_prob<double>(prob, field, P))) return rc;
@@ -1681,6 +1702,35 @@ int vpb_smpc_step(const vpb_problem *prob, const vpb_field *field, const void *e
   VPB_REQUIRE(out, "out is null");
   return smpc_launch(prob, field, eps, dtype, nominal, M, 0, precision, costs, flags, nullptr, out, workspace,
                      workspace_bytes, as_stream(stream));
+}
+
+int vpb_smpc_generate(const vpb_problem *prob, const vpb_field *field, uint64_t seed, const uint64_t *seed_dev,
+                      int64_t m_offset, int64_t window, const double *sigma, const double *nominal, int64_t M,
+                      int precision, double *costs, uint8_t *flags, void *eps_out, double *part_out, double *out,
+                      void *workspace, size_t workspace_bytes, void *stream) {
+  VPB_REQUIRE(prob && sigma && eps_out, "null argument to vpb_smpc_generate");
+  VPB_REQUIRE((part_out == nullptr) != (out == nullptr), "exactly one of part_out / out");
+  VPB_REQUIRE(window >= 1 && window <= 9, "noise window must be in [1, 9]");
+  cudaStream_t s = as_stream(stream);
+  const int64_t H = prob->horizon, n = prob->n_joints;
+  const int dtype = precision == VPB_PREC_F32 ? VPB_DTYPE_F32 : VPB_DTYPE_F64;
+  const bool fused = precision == VPB_PREC_F32 && window <= 5 && !fixed_topology_disabled() && topo_id(prob) == 1;
+  if (fused) {
+    NoiseGen g;
+    memset(&g, 0, sizeof(g));
+    g.seed = seed;
+    g.seed_dev = seed_dev;
+    g.m_offset = m_offset;
+    g.window = (int)window;
+    for (int64_t j = 0; j < n; ++j) g.sigma[j] = (float)sigma[j];
+    return smpc_launch(prob, field, eps_out, VPB_DTYPE_F32, nominal, M, m_offset, precision, costs, flags, part_out,
+                       out, workspace, workspace_bytes, s, &g);
+  }
+  // runtime topology / fp64 / wide windows: the stand-alone sampler (same draws), then the step
+  int rc = vpb_sample_perturbations(seed, seed_dev, m_offset, M, H, n, window, sigma, dtype, eps_out, stream);
+  if (rc) return rc;
+  return smpc_launch(prob, field, eps_out, dtype, nominal, M, m_offset, precision, costs, flags, part_out, out,
+                     workspace, workspace_bytes, s);
 }
 
 size_t vpb_smpc_finish_workspace_bytes(int64_t n_parts, int64_t H, int64_t n) {

@@ -3,7 +3,8 @@
 // Planner.smpc_step (vp/planner.py:594-630) with host buffers in and out: the
 // per-call block (start state, goal, seed, field pointer, warm start) is
 // written to pinned memory, one captured CUDA graph replays
-//   H2D copy of the block -> perturbation sampler -> fused SMPC step kernel
+//   H2D copy of the block -> SMPC step (vpb_smpc_generate: the perturbations
+//   are drawn inside the fused step kernel for the compiled topology)
 //   -> D2H copy of the packed result,
 // and the call returns after a stream synchronisation.  The session owns its
 // device buffers (allocated once at creation), so a step does no allocation,
@@ -47,11 +48,9 @@ int enqueue(vpb_smpc_session *s, bool copies) {
   const int64_t nom = s->dyn_len + 2;
   if (copies)
     VPB_CUDA(cudaMemcpyAsync(s->d_in, s->h_in, (size_t)s->in_len * 8, cudaMemcpyHostToDevice, s->stream));
-  int rc = vpb_sample_perturbations(0, reinterpret_cast<const uint64_t *>(s->d_in + s->dyn_len), 0, s->M, s->H, s->n,
-                                    s->window, s->sigma, s->dtype, s->eps, s->stream);
-  if (rc) return rc;
-  rc = vpb_smpc_step(&s->prob, &s->field, s->eps, s->dtype, s->d_in + nom, s->M, s->precision, nullptr, nullptr,
-                     s->d_out, s->ws, s->ws_bytes, s->stream);
+  const int rc = vpb_smpc_generate(&s->prob, &s->field, 0, reinterpret_cast<const uint64_t *>(s->d_in + s->dyn_len),
+                                   0, s->window, s->sigma, s->d_in + nom, s->M, s->precision, nullptr, nullptr, s->eps,
+                                   nullptr, s->d_out, s->ws, s->ws_bytes, s->stream);
   if (rc) return rc;
   if (copies)
     VPB_CUDA(cudaMemcpyAsync(s->h_out, s->d_out, (size_t)s->out_len * 8, cudaMemcpyDeviceToHost, s->stream));

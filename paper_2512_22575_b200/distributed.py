@@ -56,13 +56,17 @@ class ShardedSMPC:
     def step_device(self, state, goal, snap, nominal_dev: torch.Tensor, rng_seed: int,
                     perturbations: torch.Tensor | None = None) -> torch.Tensor:
         pl = self.planner
-        if perturbations is None:
-            eps = pl.sample_device(rng_seed, m_offset=self.sample_range()[0], samples=self.m_local)
+        lo = self.sample_range()[0]
+        if perturbations is None:  # draws inside the step kernel (vpb_smpc_generate)
+            res, _ = pl.smpc_generate_device(state, goal, snap, nominal_dev, rng_seed, samples=self.m_local,
+                                             m_offset=lo, partial=self.world > 1)
+            if self.world == 1:
+                return res
+            part = res
+        elif self.world == 1:
+            return pl.smpc_step_device(state, goal, snap, nominal_dev, perturbations)  # one fused launch
         else:
-            eps = perturbations
-        if self.world == 1:
-            return pl.smpc_step_device(state, goal, snap, nominal_dev, eps)  # one fused launch
-        part, _, _ = pl.smpc_partial_device(state, goal, snap, nominal_dev, eps, m_offset=self.sample_range()[0])
+            part, _, _ = pl.smpc_partial_device(state, goal, snap, nominal_dev, perturbations, m_offset=lo)
         parts = exchange_partials(part, self.world, self.group)
         return pl.smpc_finish_device(state, goal, snap, nominal_dev, parts)
 

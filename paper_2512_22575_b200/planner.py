@@ -359,6 +359,33 @@ class Planner:
               "smpc_step")
         return out
 
+    def smpc_generate_device(self, state, goal, snap, nominal_dev: torch.Tensor, rng_seed: int,
+                             samples: int | None = None, m_offset: int = 0, partial: bool = False,
+                             seed_dev: torch.Tensor | None = None, dyn: torch.Tensor | None = None,
+                             eps_out: torch.Tensor | None = None, out: torch.Tensor | None = None):
+        """Draw + step in one call (vpb_smpc_generate): the perturbations of
+        ``sample_device`` with the same seed / offset, then the fused step
+        (``partial=False``: the packed step output) or this shard's softmin
+        partial (``partial=True``).  Returns (result, eps)."""
+        p = self.params
+        m = p.samples if samples is None else int(samples)
+        h, n = p.horizon, self.chain.dof
+        P = self.problem(state, goal, horizon=h, dyn=dyn)
+        L = load()
+        if eps_out is None:
+            eps_out = torch.empty((m, h, n), dtype=self._eps_dtype, device=self.device)
+        if out is None:
+            length = L.vpb_smpc_partial_len(h, n) if partial else L.vpb_smpc_out_len(h, n)
+            out = torch.empty(int(length), dtype=torch.float64, device=self.device)
+        ws = self._smpc_ws(m, h)
+        sig = np.ascontiguousarray(np.broadcast_to(np.asarray(p.sigma, dtype=float), (n,)))
+        check(L.vpb_smpc_generate(P, _field_struct(snap), int(rng_seed) & 0xFFFFFFFFFFFFFFFF, D.ptr(seed_dev),
+                                  int(m_offset), p.noise_window, D.host_ptr(sig), D.ptr(nominal_dev), m, self._prec,
+                                  None, None, D.ptr(eps_out), D.ptr(out) if partial else None,
+                                  None if partial else D.ptr(out), D.ptr(ws), ws.numel(), D.stream(self.device)),
+              "smpc_generate")
+        return out, eps_out
+
     def smpc_finish_device(self, state, goal, snap, nominal_dev: torch.Tensor, partials: torch.Tensor,
                            dyn: torch.Tensor | None = None):
         """Merge rank partials (R, L) in rank order and finish the step on the
@@ -550,9 +577,9 @@ class SmpcGraph:
 
     def _enqueue(self, copy_out: bool):
         self.dev_in.copy_(self.host_in, non_blocking=True)
-        self.pl.sample_device(0, samples=self.m, seed_dev=self._seed_view, out=self.eps)
-        self.pl.smpc_step_device(None, None, self.snap, self._nom_view, self.eps, out=self.dev_out,
-                                 dyn=self._dyn_view)
+        self.pl.smpc_generate_device(None, None, self.snap, self._nom_view, 0, samples=self.m,
+                                     seed_dev=self._seed_view, dyn=self._dyn_view, eps_out=self.eps,
+                                     out=self.dev_out)
         if copy_out:
             self.host_out.copy_(self.dev_out, non_blocking=True)
 

@@ -449,3 +449,34 @@ def test_native_session_equals_device_step(pk, precision):
                                                                            goal.rotation.to_quaternion()),
                                    rtol=1e-9, atol=1e-12)
     assert len(pl._sessions) == 1  # one session serves both field buffers
+
+
+@pytest.mark.parametrize("precision,window", [("fp32", 5), ("fp32", 7), ("fp64", 5)])
+def test_generate_equals_sampler_plus_step(pk, precision, window):
+    """vpb_smpc_generate (draws inside the fused step kernel for the compiled
+    topology in fp32, window <= 5; sampler + step otherwise) gives the same
+    perturbations as sample_device and the same step / shard partial."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.geometry import RigidTransform
+
+    chain, model = config.robot_7dof()
+    grid = mapping.VoxelGrid((-1.0, -1.0, 0.0), 0.05, (30, 30, 30))
+    occ = np.zeros((30, 30, 30), bool)
+    occ[12:16, 12:16, 10:14] = True
+    grid.set_log_odds(np.where(occ, 3.5, 0.0))
+    field = mapping.edt_3d(grid, outside_default=0.8)
+    for m, h in ((1000, 20), (4096, 32), (300, 70)):
+        params = config.planner_params(7, {"samples": m, "horizon": h, "noise_window": window})
+        pl = planner.Planner(chain, model, params, precision)
+        state = robot.JointState(np.full(7, 0.1), np.linspace(-0.2, 0.2, 7), np.zeros(7))
+        goal = RigidTransform.from_vec7([0.3, -0.2, 0.7, 0.9, 0.1, 0.3, -0.2])
+        nom = torch.from_numpy(0.2 * np.cos(np.arange(h * 7)).reshape(h, 7)).cuda()
+        out, eps = pl.smpc_generate_device(state, goal, field, nom, 41)
+        ref_eps = pl.sample_device(41)
+        torch.testing.assert_close(eps, ref_eps, rtol=0, atol=0)
+        ref = pl.smpc_step_device(state, goal, field, nom, ref_eps)
+        torch.testing.assert_close(out, ref, rtol=0, atol=0, equal_nan=True)
+        part, _ = pl.smpc_generate_device(state, goal, field, nom, 41, m_offset=64, partial=True)
+        ref_part, _, _ = pl.smpc_partial_device(state, goal, field, nom, pl.sample_device(41, m_offset=64),
+                                                m_offset=64)
+        torch.testing.assert_close(part, ref_part, rtol=0, atol=0)
