@@ -57,6 +57,8 @@ def parse():
     ap.add_argument("--grid", type=int, default=256)
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the C1 / C5 replan measurements")
+    ap.add_argument("--c5-frames", type=int, default=100)
     return ap.parse_args()
 
 
@@ -129,6 +131,15 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def ncu_traffic() -> dict:
+    """DRAM bytes per launch of the step's kernels from the committed ncu
+    capture (profiles/r1_ncu_traffic.json, tools/ncu_traffic.py)."""
+    p = ROOT / "profiles" / "r1_ncu_traffic.json"
+    if p.exists():
+        return {k: v["bytes"] for k, v in json.loads(p.read_text()).items()}
+    return {}
+
+
 def measured_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -157,6 +168,60 @@ def make_scene(args, dev):
     goal = robot.forward_kinematics(chain, np.full(7, 0.35))[-1]
     return dict(chain=chain, model=model, centers=centers, radii=radii, grid=grid, cam=cam, depth=depth,
                 mapper=mapper, field=field, params=params, planner=pl, state=state, goal=goal, touched=touched)
+
+
+# ----------------------------------------------------------------------------- closed loop (C1, C5)
+def closed_loop(dev, dims, samples, horizon, frames, warm=3):
+    """p50 replan ms over `frames` frames of a moving-obstacle scene: per frame
+    the masked update of a rendered depth image (host render, untimed), the
+    exact EDT of the whole grid and one SMPC step through the public API
+    (native session; the field buffer changes every frame), then the
+    executed command is integrated.  SURVEY.md 8d C1 / C5."""
+    import torch
+
+    from paper_2512_22575_b200 import config, mapping, planner, robot, scene
+
+    chain, model = config.robot_7dof()
+    n = len(dims)
+    grid, cam, _ = scene.bench_edt_scene(dims, device=dev)
+    mapper = mapping.OccupancyMapper(grid, cam, outside_default=0.8)
+    extent = np.array(dims) * grid.voxel_size
+    params = config.planner_params(7, {"samples": samples, "horizon": horizon})
+    pl = planner.Planner(chain, model, params, device=dev)
+    state = robot.JointState.resting(np.full(7, 0.05))
+    goal = robot.forward_kinematics(chain, np.full(7, 0.35))[-1]
+    nominal = np.zeros((horizon, 7))
+    half = np.maximum(extent * 0.25, grid.voxel_size * 2) / 2.0
+    center = np.array([0.0, 0.0, extent[2] * 0.5])
+    depths, masks = [], []
+    for f in range(frames + warm):  # untimed inputs: a 10 cm cube sweeping past the static box
+        s_ = -1.0 + 2.0 * (f % 50) / 49.0
+        cube_c = np.array([0.4 * s_, 0.25, 0.45])
+        boxes = [(center - half, center + half), (cube_c - 0.05, cube_c + 0.05)]
+        centers, radii = robot.sphere_positions(chain, np.full(7, 0.3) + 0.01 * f, model)
+        depths.append(mapping.DepthImage(scene.render_boxes(cam, boxes, (centers, radii))))
+        masks.append((centers, radii))
+    stream = torch.cuda.current_stream(dev)
+    times = []
+    for f in range(frames + warm):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        mapper.update(depths[f], mask=masks[f])
+        field = mapper.recompute_edt()
+        res = pl.smpc_step(state, goal, field, nominal, f)
+        e1.record(stream)
+        e1.synchronize()
+        if f >= warm:
+            times.append(e0.elapsed_time(e1))
+        state = pl.integrate(state, res.command)
+        nominal = res.next_nominal
+    del n
+    return {"metric": "p50 replan ms", "value": statistics.median(times), "unit": "ms",
+            "p90": float(np.percentile(times, 90)), "frames": frames, "grid": list(dims), "samples": samples,
+            "horizon": horizon,
+            "per_frame": "masked fusion (160x120 depth, 11-sphere body mask) + exact EDT of the whole grid + "
+                         "Planner.smpc_step (host in/out); depth rendered on the host, untimed"}
 
 
 # ----------------------------------------------------------------------------- ours
@@ -252,6 +317,18 @@ def run_ours(args):
     t_roll, _ = timed(rollout_only, args.steps, args.warmup)
     ms_roll = statistics.mean(t_roll)
 
+    # the step's dominant kernel alone: the fused SMPC kernel (draws + rollout +
+    # softmin + merge + U* + re-evaluation), one launch (+ its counter memset)
+    gen_eps = torch.empty((M, H, n), dtype=torch.float32 if args.precision == "fp32" else torch.float64, device=dev)
+    gen_out = torch.empty(int(lib.vpb_smpc_out_len(H, n)), dtype=torch.float64, device=dev)
+
+    def fused_only(k):
+        pl.smpc_generate_device(state, goal, field, nominal, k, samples=M, m_offset=rank * M, eps_out=gen_eps,
+                                out=gen_out)
+
+    t_fused, _ = timed(fused_only, args.steps, args.warmup)
+    ms_fused = statistics.mean(t_fused)
+
     # --- B: map update (C2): masked fusion and EDT timed separately -----------
     depth_dev = S["depth"]
     depth_dev.device_tensor(dev)
@@ -301,9 +378,17 @@ def run_ours(args):
     fp32_peak = sm_count * 128 * 2 * clk_mhz * 1e6 / 1e12  # TFLOP/s at max clock
     roll_flops = (FLOP_PER_ROLLOUT_STEP * H + FLOP_PER_ROLLOUT_TERMINAL) * M
     roll_tflops = roll_flops / (ms_roll * 1e-3) / 1e12
+    fused_tflops = roll_flops / (ms_fused * 1e-3) / 1e12
+    traffic = ncu_traffic()
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     edt_gbs = EDT_BYTES_PER_VOXEL * vox / (ms_edt * 1e-3) / 1e9
     fus_gbs = FUSION_BYTES_PER_TOUCHED * S["touched"] / (ms_fus * 1e-3) / 1e9
+
+    configs = {}
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs["c1"] = closed_loop(dev, (64, 64, 64), 256, 20, 20)
+        configs["c5"] = closed_loop(dev, (512, 512, 512), 16384, 32, args.c5_frames)
+        torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -327,16 +412,23 @@ def run_ours(args):
                        "unit": "Mvoxel/s", "ms": ms_fus, "touched_voxels": S["touched"]},
             "replan": {"metric": "p50 replan ms (fusion + EDT 256^3 + SMPC M x H)", "value": p50_replan,
                        "unit": "ms", "launches_per_step": launches_replan / max(1, args.steps)},
-            "roofline": {"kernel": "rollout_kernel", "bound": "fp32", "achieved": roll_tflops,
-                         "peak": fp32_peak, "unit": "TFLOP/s", "frac": roll_tflops / fp32_peak, "traffic": None,
-                         "ms": ms_roll,
-                         "note": "FP32-issue-bound (SURVEY.md 8d: 2294 FLOP/rollout-step + 1217/rollout); "
-                                 "peak = SMs x 128 x 2 x sm_max_mhz"},
+            "roofline": {"kernel": "smpc_kernel (fused step: draws + rollout + softmin + U* + re-evaluation)",
+                         "bound": "fp32", "achieved": fused_tflops, "peak": fp32_peak, "unit": "TFLOP/s",
+                         "frac": fused_tflops / fp32_peak, "traffic": traffic.get("smpc_kernel"),
+                         "traffic_unit": "bytes/launch", "ms": ms_fused,
+                         "note": "FP32-issue-bound: achieved = (2294 FLOP/rollout-step x H + 1217/rollout) x M "
+                                 "(SURVEY.md 8d) / CUDA-event time of one fused launch, L2 flushed; peak = SMs x "
+                                 "128 x 2 x sm_max_mhz (no FP32 entry in MEASURED_PEAKS.json); traffic = ncu "
+                                 "dram__bytes_read+write of the kernel (profiles/r1_ncu_traffic.json)"},
             "rooflines": [
-                {"kernel": "edt (3 passes)", "bound": "hbm", "achieved": edt_gbs, "peak": hbm, "unit": "GB/s",
-                 "frac": edt_gbs / hbm, "bytes_per_voxel": EDT_BYTES_PER_VOXEL},
+                {"kernel": "rollout_kernel (evaluate_batch alone)", "bound": "fp32", "achieved": roll_tflops,
+                 "peak": fp32_peak, "unit": "TFLOP/s", "frac": roll_tflops / fp32_peak, "ms": ms_roll},
+                {"kernel": "edt (line table + Z+Y FH + X FH)", "bound": "hbm", "achieved": edt_gbs, "peak": hbm,
+                 "unit": "GB/s", "frac": edt_gbs / hbm, "bytes_per_voxel": EDT_BYTES_PER_VOXEL,
+                 "traffic": traffic.get("edt"), "traffic_unit": "bytes/call"},
                 {"kernel": "fuse+masked_pixels", "bound": "hbm", "achieved": fus_gbs, "peak": hbm, "unit": "GB/s",
-                 "frac": fus_gbs / hbm, "bytes_per_touched_voxel": FUSION_BYTES_PER_TOUCHED},
+                 "frac": fus_gbs / hbm, "bytes_per_touched_voxel": FUSION_BYTES_PER_TOUCHED,
+                 "traffic": traffic.get("fuse_kernel"), "traffic_unit": "bytes/call"},
             ],
             "e2e": {"value": world * M / (ms_e2e * 1e-3), "unit": UNIT, "ms": ms_e2e, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
@@ -348,6 +440,8 @@ def run_ours(args):
             "clocks": clocks,
             "peaks_source": "MEASURED_PEAKS.json (measured)" if not peaks.get("_fallback") else "fallback",
         }
+        if configs:
+            line["configs"] = configs
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)

@@ -18,9 +18,10 @@ def main():
     nom = torch.zeros((32, 7), dtype=torch.float64, device="cuda")
     one = torch.zeros((1, 32, 7), dtype=torch.float64, device="cuda")
     eps = pl.sample_device(3)
-    for _ in range(3):
+    for k in range(3):
         pl.evaluate_device(st, goal, field, one)
         pl.smpc_step_device(st, goal, field, nom, eps)
+        pl.smpc_generate_device(st, goal, field, nom, k)  # fused draws (the production step)
     torch.cuda.synchronize()
     print("done")
 
