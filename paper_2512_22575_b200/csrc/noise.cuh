@@ -43,7 +43,7 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 ctr, uint32_t k0, uint32_t 
 __device__ __forceinline__ void box_muller_f(uint32_t a, uint32_t b, float &z0, float &z1) {
   const float u1 = ((float)(a >> 8) + 0.5f) * 5.9604644775390625e-08f;  // (0,1), 24-bit
   const float u2 = ((float)(b >> 8) + 0.5f) * 5.9604644775390625e-08f;
-  const float r = sqrtf(-2.0f * logf(u1));
+  const float r = sqrtf(-2.0f * __logf(u1));  // MUFU.LG2; u1 in (0, 1) away from denormals
   float s, c;
   sincospif(2.0f * u2, &s, &c);
   z0 = r * c;
@@ -100,20 +100,23 @@ __device__ __forceinline__ void candidate_noise(const NoiseGen &G, int64_t m_loc
   }
   const int lo = max(0, k - back), hi = min(H, k + fwd + 1);
   const float scale = (mg == 0 || k >= H) ? 0.0f : rsqrtf((float)(hi - lo));
+  // window offsets d in use at this step (bit d + HALF), computed once
+  unsigned dmask = 0u;
+#pragma unroll
+  for (int d = -HALF; d <= HALF; ++d)
+    if (d >= -back && d <= fwd && k + d >= 0 && k + d < H) dmask |= 1u << (d + HALF);
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     float acc = 0.0f;
 #pragma unroll
     for (int d = -HALF; d <= HALF; ++d) {
       const int src = lane + d;  // lane of step k + d within the chunk (may leave [0, 32))
-      const float vm = __shfl_sync(kFull, zm[j], src & 31);
-      float v = vm;
-      if (multi) {
+      float v = __shfl_sync(kFull, zm[j], src & 31);
+      if (multi) {  // warp-uniform
         const float vh = __shfl_sync(kFull, zh[j], src < 0 ? src + 4 : (src - 28) & 31);
-        v = (src < 0 || src >= 32) ? vh : vm;
+        v = (src < 0 || src >= 32) ? vh : v;
       }
-      const int kk = k + d;
-      if (d >= -back && d <= fwd && kk >= 0 && kk < H) acc += v;
+      acc += ((dmask >> (d + HALF)) & 1u) ? v : 0.0f;
     }
     u[j] = acc * scale * G.sigma[j];
   }

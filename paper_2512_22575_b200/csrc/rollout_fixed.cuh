@@ -141,16 +141,13 @@ __device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C,
     g2 = (pz - P.origin2) * P.inv_voxel - P.lo2;
   }
   const bool inside = g0 >= T(0) && g0 < C.nf0 && g1 >= T(0) && g1 < C.nf1 && g2 >= T(0) && g2 < C.nf2;
-  if (!inside) g0 = g1 = g2 = T(0);
+  if (!inside) g0 = g1 = g2 = T(0);  // any in-range address; the result is selected away
   // c = g - 1/2 clamped to [0, n - 1] (vp/mapping.py:654-663)
   T c0 = g0 - T(0.5), c1 = g1 - T(0.5), c2 = g2 - T(0.5);
-  c0 = c0 < T(0) ? T(0) : (c0 > C.chi0 ? C.chi0 : c0);
-  c1 = c1 < T(0) ? T(0) : (c1 > C.chi1 ? C.chi1 : c1);
-  c2 = c2 < T(0) ? T(0) : (c2 > C.chi2 ? C.chi2 : c2);
-  T a0 = floor(c0), a1 = floor(c1), a2 = floor(c2);
-  a0 = a0 > C.amax0 ? C.amax0 : a0;
-  a1 = a1 > C.amax1 ? C.amax1 : a1;
-  a2 = a2 > C.amax2 ? C.amax2 : a2;
+  c0 = fmin(fmax(c0, T(0)), C.chi0);
+  c1 = fmin(fmax(c1, T(0)), C.chi1);
+  c2 = fmin(fmax(c2, T(0)), C.chi2);
+  const T a0 = fmin(floor(c0), C.amax0), a1 = fmin(floor(c1), C.amax1), a2 = fmin(floor(c2), C.amax2);
   const T f0 = c0 - a0, f1 = c1 - a1, f2 = c2 - a2;  // in [0, 1]
   const int i0 = (int)a0, i1 = (int)a1, i2 = (int)a2;
   const float *p = sq + ((i0 * P.n1 + i1) * P.n2 + i2);
@@ -161,13 +158,11 @@ __device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C,
   const float v4 = __ldg(px_), v5 = __ldg(px_ + C.off2);
   const float *pxy = px_ + C.off1;
   const float v6 = __ldg(pxy), v7 = __ldg(pxy + C.off2);
-  if (!inside) return C.out_cost[s];
   // containing cell floor(g): the b corner on an axis iff g >= a + 1
   const bool sx = g0 >= a0 + T(1), sy = g1 >= a1 + T(1), sz = g2 >= a2 + T(1);
   const float e00 = sz ? v1 : v0, e01 = sz ? v3 : v2, e10 = sz ? v5 : v4, e11 = sz ? v7 : v6;
   const float e0 = sy ? e01 : e00, e1 = sy ? e11 : e10;
   const float cell = sx ? e1 : e0;
-  if (cell == 0.0f) return C.zero_cost[s];
   const T h0 = T(1) - f0, h1 = T(1) - f1, h2 = T(1) - f2;
   const T c00 = fma((T)v4, f0, (T)v0 * h0);
   const T c01 = fma((T)v5, f0, (T)v1 * h0);
@@ -176,10 +171,18 @@ __device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C,
   const T c0v = fma(c10, f1, c00 * h1);
   const T c1v = fma(c11, f1, c01 * h1);
   const T value = fma(c1v, f2, c0v * h2);
-  if (!(value < C.thr2[s])) return T(0);  // distance >= d_act + r (also the all-inf field)
-  const T dist = P.voxel * tsqrt<T>(value);
-  const T gap = P.d_act - (dist - P.sph_r[s]);
-  return gap > T(0) ? P.w_env * gap * gap : T(0);
+  // branch-free selection (the all-inf field gives inf / NaN -> no cost)
+  T env;
+  if constexpr (sizeof(T) == 8) {
+    const T gap = P.d_act - (P.voxel * sqrt(value) - P.sph_r[s]);
+    env = gap > T(0) ? P.w_env * gap * gap : T(0);
+  } else {
+    const float dist = P.voxel * (value * rsqrtf(fmaxf(value, 1e-30f)));
+    const float gap = P.d_act - (dist - P.sph_r[s]);
+    env = gap > 0.0f ? P.w_env * gap * gap : 0.0f;
+  }
+  env = cell == 0.0f ? C.zero_cost[s] : env;
+  return inside ? env : C.out_cost[s];
 }
 
 // Which terms of a configuration one warp evaluates (warp-uniform): the
@@ -196,6 +199,7 @@ struct Split {
 template <typename Topo>
 __device__ __forceinline__ Split make_split(int sub, int nsub) {
   static_assert(Topo::NS <= 32 && Topo::NP <= 64, "split masks hold 32 spheres / 64 pairs");
+  if (nsub == 1) return Split{0xffffffffu, ~0ull, true};  // a candidate warp: everything
   Split w{0u, 0ull, sub == nsub - 1};
   for (int s = sub; s < Topo::NS; s += nsub) w.smask |= 1u << s;
   for (int p = sub; p < Topo::NP; p += nsub) w.pmask |= 1ull << p;
@@ -317,10 +321,14 @@ __device__ __forceinline__ bool fixed_config(const Prob<T> &P, const FixedConsts
       constexpr int i = Topo::pair_i(p), j = Topo::pair_j(p);
       const T dx = cx[i] - cx[j], dy = cy[i] - cy[j], dz = cz[i] - cz[j];
       const T d2 = dx * dx + dy * dy + dz * dz;
-      if (((W.pmask >> p) & 1ull) && d2 < C.rsum2[p]) {
-        const T gap = tsqrt<T>(d2) - C.rsum[p];
-        if (gap < T(0)) self += P.w_self * gap * gap;
+      T gap;
+      if constexpr (sizeof(T) == 8) {
+        gap = sqrt(d2) - C.rsum[p];
+      } else {
+        gap = d2 * rsqrtf(fmaxf(d2, 1e-30f)) - C.rsum[p];
       }
+      const T pen = gap < T(0) ? P.w_self * gap * gap : T(0);
+      self += ((W.pmask >> p) & 1ull) ? pen : T(0);
     });
   }
   coll = env + self;
