@@ -297,12 +297,17 @@ int vpb_smpc_session_create(const vpb_problem *prob, const vpb_field *field, int
 /* One step: q0, qd0 (n), goal_r (9, row major), goal_t (3), nominal (H x n,
  * NULL = zeros) and the seed are host inputs; field_sq (dev, NULL = the
  * creation-time buffer); out (host, vpb_smpc_session_out_len doubles).  The
- * graph is replayed on `stream` (NULL = the session's own stream), so it is
+ * graph is replayed on `stream` (NULL = the legacy default stream), so it is
  * ordered after the work that produced the field; the call returns when the
  * step is complete. */
 int vpb_smpc_session_step(vpb_smpc_session *session, const double *q0, const double *qd0, const double *goal_r,
                           const double *goal_t, const double *nominal, uint64_t seed, const float *field_sq,
                           double *out, void *stream);
+/* Asynchronous replay of the step graph on `stream` with the inputs staged
+ * by the previous vpb_smpc_session_step (device-side timing, pipelining);
+ * the result lands in the session's pinned buffer when the stream reaches
+ * it.  Returns without synchronising. */
+int vpb_smpc_session_launch(vpb_smpc_session *session, void *stream);
 int vpb_smpc_session_destroy(vpb_smpc_session *session);
 
 /* Step diagnostics on the host (vp/planner.py:620-629): end-effector position

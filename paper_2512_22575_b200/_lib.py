@@ -120,6 +120,7 @@ SIGNATURES = {
     "vpb_smpc_session_create": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _i64, _i64, _p, ctypes.c_int,
                                                _P(_p)]),
     "vpb_smpc_session_step": (ctypes.c_int, [_p, _p, _p, _p, _p, _p, ctypes.c_uint64, _p, _p, _p]),
+    "vpb_smpc_session_launch": (ctypes.c_int, [_p, _p]),
     "vpb_smpc_session_destroy": (ctypes.c_int, [_p]),
     "vpb_ee_errors": (ctypes.c_int, [_P(VpbProblem), _p, _p, _p, _p, _p]),
 }

@@ -801,6 +801,7 @@ struct SmpcIO {
   NoiseGen gen;    // on-the-fly perturbations (fixed path) when gen_on
   int gen_on;
   float *eps_out;  // where the drawn perturbations go (== eps for the merge)
+  double *out_host;  // optional host-mapped copy of `out`, written by the last CTA at the end
 };
 
 // U* = nominal + N / Z, the clipped command and the shifted warm start
@@ -1107,7 +1108,14 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
     CandOut co{nullptr, nullptr, nullptr};
     evaluate_cta<T, ET, MAXJ>(P, D, eps, io.nominal, io.M, cta_m0, S, co);
     if (!cta_reduce_and_merge<ET, smpc_nw<Topo>()>(io, S, cta_m0, hn, blockIdx.x, gridDim.x)) return;
-    if (io.finish) smpc_tail_dyn<T, MAXJ>(P, D, io.rank_part, io.nominal, io.acc, io.out, S);
+    if (io.finish) {
+      smpc_tail_dyn<T, MAXJ>(P, D, io.rank_part, io.nominal, io.acc, io.out, S);
+      if (io.out_host) {
+        __syncthreads();
+        const int len = 2 * P.H * P.nj + P.nj + 13;
+        for (int e = threadIdx.x; e < len; e += blockDim.x) io.out_host[e] = io.out[e];
+      }
+    }
   } else {
     if (blockIdx.x > 0) VPB_TRACE(io, 2 * (blockIdx.x - 1));
     // One call site, three uses: state 0 -- block 0 computes the q_0
@@ -1152,6 +1160,7 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
       if (!cta_reduce_and_merge<ET, smpc_nw<Topo>()>(io, S, cm0, hn, cta, ncta)) return;
       if (threadIdx.x == 0) {  // wait for the prologue block (normally long done)
         while (ld_acquire_gpu(pro_ready) == 0u) __nanosleep(64);
+        *pro_ready = 0u;  // counters return to zero for the next launch
       }
       __syncthreads();
       if (threadIdx.x < 32) {  // q_0 terms, summed in fixed split order
@@ -1200,6 +1209,11 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
     const double best = bad ? dinf() : io.rank_part[0] + S.pro[0] + S.pro[1];
     tail_output(S, io.rank_part, P.H, P.nj, best, bad ? (double)io.M : io.rank_part[2], io.out);
     fixed_shard_fixup(S, io.M, io.costs, io.flags, nullptr);
+    if (io.out_host) {  // zero-copy result: posted PCIe writes, visible after the kernel completes
+      __syncthreads();
+      const int len = 2 * P.H * P.nj + P.nj + 13;
+      for (int e = threadIdx.x; e < len; e += blockDim.x) io.out_host[e] = io.out[e];
+    }
     VPB_TRACE(io, 2 * ncta + 2);
   }
 }
@@ -1638,7 +1652,8 @@ int64_t vpb_smpc_out_len(int64_t H, int64_t n) { return 2 * H * n + n + 13; }
 static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const void *eps, int dtype,
                        const double *nominal, int64_t M, int64_t m_offset, int precision, double *costs,
                        uint8_t *flags, double *part_out, double *out, void *workspace, size_t workspace_bytes,
-                       cudaStream_t s, const NoiseGen *gen = nullptr) {
+                       cudaStream_t s, const NoiseGen *gen = nullptr, bool counters_zeroed = false,
+                       double *out_host = nullptr) {
   int rc = prob_checks(prob, precision, dtype);
   if (rc) return rc;
   VPB_REQUIRE(eps && nominal && M >= 1, "bad arguments to the SMPC step");
@@ -1649,7 +1664,7 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   VPB_REQUIRE(workspace && workspace_bytes >= w.bytes, "workspace too small");
   const int64_t ctas = ceil_div(M, NWF);
   const int64_t groups = ceil_div(ctas, kGroup);
-  VPB_CUDA(cudaMemsetAsync(w.counters, 0, (size_t)(groups + 2) * 4, s));
+  if (!counters_zeroed) VPB_CUDA(cudaMemsetAsync(w.counters, 0, (size_t)(groups + 2) * 4, s));
   SmpcIO io;
   memset(&io, 0, sizeof(io));
   io.eps = eps;
@@ -1670,6 +1685,7 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   io.acc = acc_of(prob);
   io.dyn = prob->dyn_state;
   io.trace = g_smpc_trace;
+  io.out_host = out_host;
   const int topo = fixed_topology_disabled() ? 0 : topo_id(prob);
   if (gen) {  // fused draw (eps is the output buffer of the draws)
     io.gen = *gen;
@@ -1732,6 +1748,38 @@ int vpb_smpc_generate(const vpb_problem *prob, const vpb_field *field, uint64_t 
   return smpc_launch(prob, field, eps_out, dtype, nominal, M, m_offset, precision, costs, flags, part_out, out,
                      workspace, workspace_bytes, s);
 }
+
+}  // extern "C"
+
+namespace vpb {
+// Session variant of vpb_smpc_generate (single-device step): the workspace's
+// counters are zero on entry (zeroed once at session creation; every launch
+// returns them to zero), and the result is also written to a host-mapped
+// buffer by the kernel itself -- no memset and no D2H copy node.
+int smpc_generate_session(const vpb_problem *prob, const vpb_field *field, const uint64_t *seed_dev, int64_t window,
+                          const double *sigma, const double *nominal, int64_t M, int precision, void *eps_out,
+                          double *out, double *out_host, void *workspace, size_t workspace_bytes,
+                          cudaStream_t s) {
+  const int64_t n = prob->n_joints;
+  const bool fused = precision == VPB_PREC_F32 && window <= 5 && !fixed_topology_disabled() && topo_id(prob) == 1;
+  if (fused) {
+    NoiseGen g;
+    memset(&g, 0, sizeof(g));
+    g.seed_dev = seed_dev;
+    g.window = (int)window;
+    for (int64_t j = 0; j < n; ++j) g.sigma[j] = (float)sigma[j];
+    return smpc_launch(prob, field, eps_out, VPB_DTYPE_F32, nominal, M, 0, precision, nullptr, nullptr, nullptr, out,
+                       workspace, workspace_bytes, s, &g, true, out_host);
+  }
+  const int dtype = precision == VPB_PREC_F32 ? VPB_DTYPE_F32 : VPB_DTYPE_F64;
+  int rc = vpb_sample_perturbations(0, seed_dev, 0, M, prob->horizon, n, window, sigma, dtype, eps_out, s);
+  if (rc) return rc;
+  return smpc_launch(prob, field, eps_out, dtype, nominal, M, 0, precision, nullptr, nullptr, nullptr, out, workspace,
+                     workspace_bytes, s, nullptr, true, out_host);
+}
+}  // namespace vpb
+
+extern "C" {
 
 size_t vpb_smpc_finish_workspace_bytes(int64_t n_parts, int64_t H, int64_t n) {
   (void)n_parts;

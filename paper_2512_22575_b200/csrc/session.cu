@@ -3,9 +3,9 @@
 // Planner.smpc_step (vp/planner.py:594-630) with host buffers in and out: the
 // per-call block (start state, goal, seed, field pointer, warm start) is
 // written to pinned memory, one captured CUDA graph replays
-//   H2D copy of the block -> SMPC step (vpb_smpc_generate: the perturbations
-//   are drawn inside the fused step kernel for the compiled topology)
-//   -> D2H copy of the packed result,
+//   H2D copy of the block -> SMPC step (the perturbations are drawn inside
+//   the fused step kernel for the compiled topology; the kernel's last CTA
+//   writes the packed result straight into pinned host memory),
 // and the call returns after a stream synchronisation.  The session owns its
 // device buffers (allocated once at creation), so a step does no allocation,
 // no attribute setting and no per-kernel host work.
@@ -48,13 +48,10 @@ int enqueue(vpb_smpc_session *s, bool copies) {
   const int64_t nom = s->dyn_len + 2;
   if (copies)
     VPB_CUDA(cudaMemcpyAsync(s->d_in, s->h_in, (size_t)s->in_len * 8, cudaMemcpyHostToDevice, s->stream));
-  const int rc = vpb_smpc_generate(&s->prob, &s->field, 0, reinterpret_cast<const uint64_t *>(s->d_in + s->dyn_len),
-                                   0, s->window, s->sigma, s->d_in + nom, s->M, s->precision, nullptr, nullptr, s->eps,
-                                   nullptr, s->d_out, s->ws, s->ws_bytes, s->stream);
-  if (rc) return rc;
-  if (copies)
-    VPB_CUDA(cudaMemcpyAsync(s->h_out, s->d_out, (size_t)s->out_len * 8, cudaMemcpyDeviceToHost, s->stream));
-  return VPB_OK;
+  // the step kernel writes the result straight into the pinned host buffer
+  return vpb::smpc_generate_session(&s->prob, &s->field, reinterpret_cast<const uint64_t *>(s->d_in + s->dyn_len),
+                                    s->window, s->sigma, s->d_in + nom, s->M, s->precision, s->eps, s->d_out,
+                                    s->h_out, s->ws, s->ws_bytes, s->stream);
 }
 
 // 3x3 row-major helpers (host, double)
@@ -177,6 +174,7 @@ int vpb_smpc_session_create(const vpb_problem *prob, const vpb_field *field, int
   SESSION_CUDA(cudaMalloc(&s->d_out, (size_t)s->out_len * 8));
   SESSION_CUDA(cudaMalloc(&s->eps, eps_bytes));
   SESSION_CUDA(cudaMalloc(&s->ws, s->ws_bytes));
+  SESSION_CUDA(cudaMemset(s->ws, 0, s->ws_bytes));  // counters: zero once, every launch returns them to zero
   memset(s->h_in, 0, (size_t)s->in_len * 8);
   // identity goal so the warm-up launch evaluates a regular pose
   s->h_in[2 * s->n + 0] = s->h_in[2 * s->n + 4] = s->h_in[2 * s->n + 8] = 1.0;
@@ -230,17 +228,25 @@ int vpb_smpc_session_step(vpb_smpc_session *s, const double *q0, const double *q
     memcpy(h + s->dyn_len + 2, nominal, (size_t)s->H * n * 8);
   else
     memset(h + s->dyn_len + 2, 0, (size_t)s->H * n * 8);
-  // replayed on the caller's stream: ordered after whatever produced the field
-  cudaStream_t st = stream ? vpb::as_stream(stream) : s->stream;
+  // replayed on the caller's stream (NULL = the legacy default stream, as
+  // everywhere in this ABI): ordered after whatever produced the field
+  cudaStream_t st = vpb::as_stream(stream);
   VPB_CUDA(cudaGraphLaunch(s->exec, st));
   double e_pos = 0.0, e_ori = 0.0;  // host diagnostics while the step runs
   vpb_ee_errors(&s->prob, q0, goal_r, goal_t, &e_pos, &e_ori);
   VPB_CUDA(cudaStreamSynchronize(st));
-  vpb::note_launch(2);
+  vpb::note_launch(1);
   memcpy(out, s->h_out, (size_t)s->out_len * 8);
   const int64_t base = 2 * s->H * n + n;
   out[base + 11] = e_pos;
   out[base + 12] = e_ori;
+  return VPB_OK;
+}
+
+int vpb_smpc_session_launch(vpb_smpc_session *s, void *stream) {
+  VPB_REQUIRE(s, "null session");
+  VPB_CUDA(cudaGraphLaunch(s->exec, vpb::as_stream(stream)));
+  vpb::note_launch(1);
   return VPB_OK;
 }
 

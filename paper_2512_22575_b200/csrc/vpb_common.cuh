@@ -41,6 +41,13 @@ constexpr unsigned kFull = 0xffffffffu;
 // Number of SMs of the current device (cached per process).
 int sm_count();
 
+// Session step (rollout.cu): counters pre-zeroed, result also written to a
+// host-mapped buffer by the kernel (session.cu).
+int smpc_generate_session(const vpb_problem *prob, const vpb_field *field, const uint64_t *seed_dev, int64_t window,
+                          const double *sigma, const double *nominal, int64_t M, int precision, void *eps_out,
+                          double *out, double *out_host, void *workspace, size_t workspace_bytes,
+                          cudaStream_t s);
+
 }  // namespace vpb
 
 #define VPB_REQUIRE(cond, ...)      \

@@ -226,6 +226,7 @@ class Planner:
         self._acc_limits = chain.acceleration_limits()
         self._base = pack_problem(chain, model, params)
         self._sessions: dict = {}
+        self._last_session = None
 
     def problem(self, state: JointState | None, goal: RigidTransform | None, horizon: int | None = None,
                 dyn: torch.Tensor | None = None) -> VpbProblem:
@@ -453,12 +454,16 @@ class Planner:
         """The cached native step session for this field geometry."""
         f = _field_of(snap)
         m = int(samples or self.params.samples)
+        last = self._last_session
+        if last is not None and last[0] is f and last[1] == m:  # same field object: no key building
+            return last[2]
         key = (m, None if f is None else (tuple(f.volume.lo), f.volume.shape, tuple(np.asarray(f.origin).tolist()),
                                          float(f.voxel_size), float(f.outside_default), str(f.sq_device.device)))
         sess = self._sessions.get(key)
         if sess is None:
             sess = SmpcSession(self, snap, m)
             self._sessions[key] = sess
+        self._last_session = (f, m, sess)
         return sess
 
     def integrate(self, state: JointState, command: np.ndarray) -> JointState:
@@ -605,6 +610,11 @@ class SmpcGraph:
         return self.pl.unpack_step(self.host_out.numpy().copy(), state, goal, self.h)
 
 
+def _raw_stream(device_index: int) -> int:
+    """Current CUDA stream handle of the device (the cheap torch binding)."""
+    return torch._C._cuda_getCurrentRawStream(device_index)
+
+
 class SmpcSession:
     """Native single-device step (``vpb_smpc_session_*``): the per-call block
     goes to pinned memory, one captured CUDA graph runs H2D -> sampler ->
@@ -630,25 +640,35 @@ class SmpcSession:
         self._qd0 = np.zeros(self.n)
         self._gr = np.zeros(9)
         self._gt = np.zeros(3)
+        # the per-step call passes plain integers (no per-call ctypes objects)
+        self._p_q0, self._p_qd0 = self._q0.ctypes.data, self._qd0.ctypes.data
+        self._p_gr, self._p_gt, self._p_out = self._gr.ctypes.data, self._gt.ctypes.data, self.out.ctypes.data
+        self._step = L.vpb_smpc_session_step
+        self._dev_index = planner.device.index if planner.device.index is not None else torch.cuda.current_device()
 
     def step(self, state: JointState, goal: RigidTransform, nominal: np.ndarray, rng_seed: int, snap) -> StepResult:
         n = self.n
-        q0 = np.asarray(state.q, dtype=np.float64).reshape(-1)
-        qd0 = np.asarray(state.qd, dtype=np.float64).reshape(-1)
+        q0, qd0 = state.q, state.qd
         if q0.shape != (n,) or qd0.shape != (n,):
             raise DimensionMismatch("state does not match the chain's dof")
         self._q0[:] = q0
         self._qd0[:] = qd0
-        self._gr[:] = np.asarray(goal.rotation.matrix, dtype=np.float64).reshape(-1)
-        self._gt[:] = np.asarray(goal.translation, dtype=np.float64).reshape(-1)
-        nom = np.ascontiguousarray(nominal, dtype=np.float64)
+        self._gr[:] = goal.rotation.matrix.reshape(-1)
+        self._gt[:] = goal.translation
+        nom = nominal if (nominal.dtype == np.float64 and nominal.flags.c_contiguous) else \
+            np.ascontiguousarray(nominal, dtype=np.float64)
         f = _field_of(snap)
-        sq = D.ptr(f.sq_device) if f is not None else None
-        check(self._lib.vpb_smpc_session_step(self._h, D.host_ptr(self._q0), D.host_ptr(self._qd0),
-                                              D.host_ptr(self._gr), D.host_ptr(self._gt), D.host_ptr(nom),
-                                              int(rng_seed) & 0xFFFFFFFFFFFFFFFF, sq, D.host_ptr(self.out),
-                                              D.stream(self.pl.device)), "smpc_session_step")
+        sq = f.sq_device.data_ptr() if f is not None else None
+        rc = self._step(self._h, self._p_q0, self._p_qd0, self._p_gr, self._p_gt, nom.ctypes.data,
+                        int(rng_seed) & 0xFFFFFFFFFFFFFFFF, sq, self._p_out, _raw_stream(self._dev_index))
+        if rc:
+            check(rc, "smpc_session_step")
         return self.pl.unpack_step(self.out, state, goal, self.h)
+
+    def launch(self) -> None:
+        """Replay the step graph asynchronously with the last staged inputs
+        (device-side timing); the result is read by the next ``step``."""
+        check(self._lib.vpb_smpc_session_launch(self._h, D.stream(self.pl.device)), "smpc_session_launch")
 
     def __del__(self):
         h = getattr(self, "_h", None)
