@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1 / C5 replan measurements")
     ap.add_argument("--c5-frames", type=int, default=100)
+    ap.add_argument("--dist-backend", default="nccl",
+                    help="nccl (one GPU per rank); gloo lets several ranks share one GPU to exercise the sharded "
+                         "path on a 1-GPU box")
     return ap.parse_args()
 
 
@@ -234,10 +237,15 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend != "nccl":
+        local = local % torch.cuda.device_count()  # ranks may share a device (path check, not a measurement)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
     S = make_scene(args, dev)
     pl, state, goal, field, mapper = S["planner"], S["state"], S["goal"], S["field"], S["mapper"]
     M, H, n = args.samples, args.horizon, 7
@@ -300,6 +308,18 @@ def run_ours(args):
 
         def smpc_iteration(seed):
             graph.launch()
+    elif args.dist_backend == "nccl":
+        # one CUDA graph per rank: draw + rollout + shard partial, NCCL
+        # all-gather, rank-order merge + tail (eager fallback if capture fails)
+        try:
+            graph = distributed.ShardedGraph(sharded, field)
+            graph.stage(state, goal, None, 0)
+
+            def smpc_iteration(seed):
+                graph.replay()
+        except Exception as exc:  # pragma: no cover - depends on the NCCL build
+            graph = None
+            print(f"sharded graph capture failed, eager step: {exc}", file=sys.stderr)
     with ClockSampler(gpu_index) as clk:
         t_smpc, launches_smpc = timed(smpc_iteration, args.steps, args.warmup)
     clocks = clk.summary()
@@ -308,7 +328,8 @@ def run_ours(args):
     t_direct, _ = timed(lambda k: sharded.step_device(state, goal, field, nominal, k), args.steps, args.warmup)
     ms_direct = max_over_ranks(statistics.mean(t_direct))
     if graph is not None:
-        launches_smpc = args.steps  # one fused SMPC kernel per replay (inside the graph)
+        # per replay: the fused SMPC kernel (N=1); fused partial + finish kernels (N>1)
+        launches_smpc = args.steps * (1 if world == 1 else 2)
 
     # rollout kernel alone (dominant kernel) for the roofline
     eps = pl.sample_device(7, m_offset=rank * M, samples=M)
@@ -433,7 +454,8 @@ def run_ours(args):
                     "d2h_bytes_per_step": d2h,
                     "api": "Planner.smpc_step (N=1: native session, vpb_smpc_session_step) / ShardedSMPC.step "
                            "(N>1): host state / goal / nominal in, StepResult out"},
-            "launch_mode": "native session CUDA graph" if graph is not None else "direct",
+            "launch_mode": ("native session CUDA graph" if world == 1 else "per-rank CUDA graph with NCCL all-gather")
+                           if graph is not None else "direct",
             "direct_launch_ms_per_step": ms_direct,
             "gpu_launches": int(launches_smpc),
             "clocks": clocks,

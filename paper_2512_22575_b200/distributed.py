@@ -27,6 +27,9 @@ def exchange_partials(part: torch.Tensor, world: int, group=None) -> torch.Tenso
     """All-gather one partial per rank -> (world, L) in rank order."""
     if world == 1:
         return part.reshape(1, -1)
+    if part.is_cuda and dist.get_backend(group) != "nccl":  # e.g. gloo: gather through the host
+        host = exchange_partials(part.cpu(), world, group)
+        return host.to(part.device)
     out = torch.empty(world * part.numel(), dtype=part.dtype, device=part.device)
     dist.all_gather_into_tensor(out, part.contiguous(), group=group)
     return out.reshape(world, -1)
@@ -78,3 +81,78 @@ class ShardedSMPC:
         nom_dev = torch.from_numpy(nom).to(pl.device, non_blocking=True)
         out = self.step_device(state, goal, snap, nom_dev, rng_seed)
         return pl.unpack_step(out.cpu().numpy(), state, goal, h)
+
+
+class ShardedGraph:
+    """One rank's sharded SMPC step captured as a CUDA graph: H2D of the
+    per-call block, the fused draw + rollout + shard-partial kernel, the NCCL
+    all-gather of the partial records, the rank-order merge + tail kernel and
+    the D2H of the result -- one replay per step, no per-launch host work.
+    Raises if the process group cannot be captured (the caller falls back to
+    the eager ``ShardedSMPC.step_device``)."""
+
+    def __init__(self, sharded: ShardedSMPC, snap):
+        from ._lib import load
+
+        self.sh = sharded
+        pl = sharded.planner
+        self.pl, self.snap = pl, snap
+        p = pl.params
+        self.h, self.n = p.horizon, pl.chain.dof
+        dev = pl.device
+        L = load()
+        self.dyn_len = 2 * self.n + 12
+        self.block_len = self.dyn_len + 1 + self.h * self.n
+        self.host_in = torch.zeros(self.block_len, dtype=torch.float64).pin_memory()
+        self.dev_in = torch.zeros(self.block_len, dtype=torch.float64, device=dev)
+        self._seed_view = self.dev_in[self.dyn_len:self.dyn_len + 1].view(torch.int64)
+        self._nom_view = self.dev_in[self.dyn_len + 1:].view(self.h, self.n)
+        self._dyn_view = self.dev_in[:self.dyn_len]
+        self.part = torch.empty(int(L.vpb_smpc_partial_len(self.h, self.n)), dtype=torch.float64, device=dev)
+        self.parts = torch.empty(sharded.world * self.part.numel(), dtype=torch.float64, device=dev)
+        self.out = torch.empty(int(L.vpb_smpc_out_len(self.h, self.n)), dtype=torch.float64, device=dev)
+        self.host_out = torch.zeros(self.out.numel(), dtype=torch.float64).pin_memory()
+        self.eps = torch.empty((sharded.m_local, self.h, self.n), dtype=pl._eps_dtype, device=dev)
+        for _ in range(2):  # warm: workspaces, kernel attributes, NCCL communicator
+            self._enqueue(copy_out=False)
+        torch.cuda.synchronize(dev)
+        self.graph = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=dev)
+        s.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(self.graph, stream=s):
+                self._enqueue(copy_out=True)
+        torch.cuda.current_stream(dev).wait_stream(s)
+        torch.cuda.synchronize(dev)
+
+    def _enqueue(self, copy_out: bool):
+        sh, pl = self.sh, self.pl
+        self.dev_in.copy_(self.host_in, non_blocking=True)
+        pl.smpc_generate_device(None, None, self.snap, self._nom_view, 0, samples=sh.m_local,
+                                m_offset=sh.sample_range()[0], partial=True, seed_dev=self._seed_view,
+                                dyn=self._dyn_view, eps_out=self.eps, out=self.part)
+        dist.all_gather_into_tensor(self.parts, self.part, group=sh.group)
+        pl.smpc_finish_device(None, None, self.snap, self._nom_view, self.parts.view(sh.world, -1),
+                              dyn=self._dyn_view, out=self.out)
+        if copy_out:
+            self.host_out.copy_(self.out, non_blocking=True)
+
+    def stage(self, state, goal, nominal, rng_seed: int) -> None:
+        n = self.n
+        h = self.host_in.numpy()
+        h[:n] = np.asarray(state.q, dtype=float)
+        h[n:2 * n] = np.asarray(state.qd, dtype=float)
+        h[2 * n:2 * n + 9] = np.asarray(goal.rotation.matrix, dtype=float).reshape(-1)
+        h[2 * n + 9:2 * n + 12] = np.asarray(goal.translation, dtype=float)
+        h[self.dyn_len:self.dyn_len + 1].view(np.uint64)[0] = np.uint64(int(rng_seed) & 0xFFFFFFFFFFFFFFFF)
+        nom = np.zeros((self.h, n)) if nominal is None else np.asarray(nominal, dtype=float)
+        h[self.dyn_len + 1:] = nom.reshape(-1)
+
+    def replay(self) -> None:
+        self.graph.replay()
+
+    def step(self, state, goal, nominal, rng_seed: int) -> StepResult:
+        self.stage(state, goal, nominal, rng_seed)
+        self.graph.replay()
+        torch.cuda.current_stream(self.pl.device).synchronize()
+        return self.pl.unpack_step(self.host_out.numpy().copy(), state, goal, self.h)

@@ -388,13 +388,14 @@ class Planner:
         return out, eps_out
 
     def smpc_finish_device(self, state, goal, snap, nominal_dev: torch.Tensor, partials: torch.Tensor,
-                           dyn: torch.Tensor | None = None):
+                           dyn: torch.Tensor | None = None, out: torch.Tensor | None = None):
         """Merge rank partials (R, L) in rank order and finish the step on the
         device.  Returns the packed output vector (vpb_smpc_out_len)."""
         h, n = nominal_dev.shape
         P = self.problem(state, goal, horizon=h, dyn=dyn)
         L = load()
-        out = torch.empty(int(L.vpb_smpc_out_len(h, n)), dtype=torch.float64, device=self.device)
+        if out is None:
+            out = torch.empty(int(L.vpb_smpc_out_len(h, n)), dtype=torch.float64, device=self.device)
         parts = partials.reshape(-1, int(L.vpb_smpc_partial_len(h, n))).contiguous()
         ws_bytes = int(L.vpb_smpc_finish_workspace_bytes(parts.shape[0], h, n))
         ws = D.Workspace.get(self.device, "smpc_finish", ws_bytes)

@@ -480,3 +480,46 @@ def test_generate_equals_sampler_plus_step(pk, precision, window):
         ref_part, _, _ = pl.smpc_partial_device(state, goal, field, nom, pl.sample_device(41, m_offset=64),
                                                 m_offset=64)
         torch.testing.assert_close(part, ref_part, rtol=0, atol=0)
+
+
+def test_sharded_graph_nccl_world1_equals_step(pk):
+    """The per-rank CUDA graph of the sharded step (fused draw + shard partial,
+    NCCL all-gather captured in the graph, rank-order merge + tail) on a
+    one-rank NCCL group gives the single-device step."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200 import distributed
+    from paper_2512_22575_b200.geometry import RigidTransform
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        chain, model = config.robot_7dof()
+        grid = mapping.VoxelGrid((-1.0, -1.0, 0.0), 0.05, (30, 30, 30))
+        occ = np.zeros((30, 30, 30), bool)
+        occ[12:16, 12:16, 10:14] = True
+        grid.set_log_odds(np.where(occ, 3.5, 0.0))
+        field = mapping.edt_3d(grid, outside_default=0.8)
+        params = config.planner_params(7, {"samples": 2048, "horizon": 32})
+        pl = planner.Planner(chain, model, params, "fp32")
+        sh = distributed.ShardedSMPC(pl, world=1, rank=0)
+        g = distributed.ShardedGraph(sh, field)
+        state = robot.JointState(np.full(7, 0.1), np.linspace(-0.2, 0.2, 7), np.zeros(7))
+        goal = RigidTransform.from_vec7([0.3, -0.2, 0.7, 0.9, 0.1, 0.3, -0.2])
+        nom = 0.2 * np.cos(np.arange(32 * 7)).reshape(32, 7)
+        for seed in (3, 4):
+            got = g.step(state, goal, nom, seed)
+            want = pl.smpc_step(state, goal, field, nom, seed)
+            np.testing.assert_allclose(got.command, want.command, rtol=1e-12, atol=1e-14)
+            np.testing.assert_allclose(got.next_nominal, want.next_nominal, rtol=1e-12, atol=1e-14)
+            np.testing.assert_allclose(got.diagnostics.best_cost, want.diagnostics.best_cost, rtol=1e-12)
+            np.testing.assert_allclose(got.diagnostics.weighted_cost, want.diagnostics.weighted_cost, rtol=1e-12)
+    finally:
+        dist.destroy_process_group()
