@@ -352,6 +352,7 @@ def run_ours(args):
     t_fused, _ = timed(fused_only, args.steps, args.warmup)
     ms_fused = statistics.mean(t_fused)
 
+
     # --- B: map update (C2): masked fusion and EDT timed separately -----------
     depth_dev = S["depth"]
     depth_dev.device_tensor(dev)

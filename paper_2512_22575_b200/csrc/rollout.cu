@@ -802,6 +802,7 @@ struct SmpcIO {
   int gen_on;
   float *eps_out;  // where the drawn perturbations go (== eps for the merge)
   double *out_host;  // optional host-mapped copy of `out`, written by the last CTA at the end
+  double *cand_terms;  // [M][6] per-candidate sums (fixed path): the re-evaluation shortcut
 };
 
 // U* = nominal + N / Z, the clipped command and the shifted warm start
@@ -903,25 +904,46 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   int *clist = reinterpret_cast<int *>(io.group_parts + io.M + 64) + io.M + 64;  // nonzero CTAs, per-warp slices
   const double inv_lam = 1.0 / io.lam;
   // 1. global minimum over the CTA heads (first CTA attaining it)
+  constexpr int kHR = 8;  // heads kept in registers per lane (ctas <= nw * 32 * kHR)
   const int span = ((ctas + nw - 1) / nw + 31) & ~31;
   const int w0 = warp * span, w1 = min(ctas, w0 + span);
+  const bool in_regs = span <= 32 * kHR;
+  double hv[kHR];
   double mn = dinf();
   int bidx = 0x7fffffff;
   double nf = 0.0;
-  for (int c = w0; c < w1; c += 32 * 4) {
-    double v[4], f[4];
+  if (in_regs) {
+    double fv[kHR];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int i = c + 32 * t + lane;
-      v[t] = i < w1 ? heads[i] : dinf();
-      f[t] = i < w1 ? heads[ctas + i] : 0.0;
+    for (int t = 0; t < kHR; ++t) {
+      const int i = w0 + 32 * t + lane;
+      hv[t] = i < w1 ? heads[i] : dinf();
+      fv[t] = i < w1 ? heads[ctas + i] : 0.0;
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      nf += f[t];
-      if (v[t] < mn) {
-        mn = v[t];
-        bidx = c + 32 * t + lane;
+    for (int t = 0; t < kHR; ++t) {
+      nf += fv[t];
+      if (hv[t] < mn) {
+        mn = hv[t];
+        bidx = w0 + 32 * t + lane;
+      }
+    }
+  } else {
+    for (int c = w0; c < w1; c += 32 * 4) {
+      double v[4], f[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int i = c + 32 * t + lane;
+        v[t] = i < w1 ? heads[i] : dinf();
+        f[t] = i < w1 ? heads[ctas + i] : 0.0;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        nf += f[t];
+        if (v[t] < mn) {
+          mn = v[t];
+          bidx = c + 32 * t + lane;
+        }
       }
     }
   }
@@ -962,44 +984,59 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   // 2. (all warps) CTAs with a nonzero weight, compacted in order into this
   //    warp's slice of clist (cheap exponent pre-check; exp only near the min)
   int wn = 0;
-  for (int c = w0; c < w1; c += 32) {
-    const int i = c + lane;
-    const double v = i < w1 ? heads[i] : dinf();
+  auto consider = [&](int i, double v) {
     const double x = (v - m0) * inv_lam;
     const bool nz = v < dinf() && x < 746.0 && exp(-x) != 0.0;
     const unsigned bal = __ballot_sync(kFull, nz);
     if (nz) clist[w0 + wn + __popc(bal & ((1u << lane) - 1u))] = i;
     wn += __popc(bal);
+  };
+  if (in_regs) {
+#pragma unroll
+    for (int t = 0; t < kHR; ++t) consider(w0 + 32 * t + lane, hv[t]);
+  } else {
+    for (int c = w0; c < w1; c += 32) {
+      const int i = c + lane;
+      consider(i, i < w1 ? heads[i] : dinf());
+    }
   }
   if (lane == 0) misc[16 + warp] = (double)wn;
   __syncthreads();
   if (tid < 32) {
     // 3. (warp 0) the candidates of those CTAs, in order: weights and Z
+    // candidates of the nonzero CTAs over the concatenated warp slices, 32
+    // at a time: one load round trip per 32 candidates
+    int off[16];
+    int total = 0;
+    for (int w = 0; w < nw; ++w) {
+      off[w] = total;
+      total += (int)misc[16 + w] * NWC;
+    }
     int ncand = 0;
     double z = 0.0;
-    for (int w = 0; w < nw; ++w) {
-      const int cnt = (int)misc[16 + w] * NWC;
-      const int *cl = clist + w * span;
-      for (int k0 = 0; k0 < cnt; k0 += 32) {
-        const int k = k0 + lane;
-        int m = -1;
-        double wt = 0.0;
-        if (k < cnt) {
-          m = cl[k / NWC] * NWC + (k % NWC);
-          if (m < io.M) {
-            const double c = costs[m];
-            wt = c < dinf() ? exp(-(c - m0) * inv_lam) : 0.0;
-          }
+    for (int k0 = 0; k0 < total; k0 += 32) {
+      const int k = k0 + lane;
+      int m = -1;
+      double wt = 0.0;
+      if (k < total) {
+        int w = 0;
+        for (int u = 1; u < nw; ++u)
+          if (k >= off[u]) w = u;
+        const int r = k - off[w];
+        m = clist[w * span + r / NWC] * NWC + (r % NWC);
+        if (m < io.M) {
+          const double c = costs[m];
+          wt = c < dinf() ? exp(-(c - m0) * inv_lam) : 0.0;
         }
-        const unsigned bal = __ballot_sync(kFull, wt != 0.0);
-        if (wt != 0.0) {
-          const int p = ncand + __popc(bal & ((1u << lane) - 1u));
-          mlist[p] = m;
-          wlist[p] = wt;
-        }
-        z += wt;  // lane-strided partials in candidate order
-        ncand += __popc(bal);
       }
+      const unsigned bal = __ballot_sync(kFull, wt != 0.0);
+      if (wt != 0.0) {
+        const int p = ncand + __popc(bal & ((1u << lane) - 1u));
+        mlist[p] = m;
+        wlist[p] = wt;
+      }
+      z += wt;  // lane-strided partials in candidate order
+      ncand += __popc(bal);
     }
     z = warp_sum_d(z);
     if (lane == 0) {
@@ -1010,6 +1047,7 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
       dst[2] = misc[43];
       dst[3] = (b0 >= 0 && b0 < ctas) ? heads[2 * (size_t)ctas + b0] : -1.0;
       misc[42] = (double)ncand;
+      misc[45] = ncand == 1 ? (double)mlist[0] : -1.0;  // the only nonzero weight (U* = nominal + its eps)
     }
   }
   __syncthreads();
@@ -1052,6 +1090,11 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
       c = failed ? dinf() : sm[0] + sm[1] + sm[2] + sm[3] + sm[4] + S.cost[w];
       costs[m] = c;
       if (io.flags) io.flags[m] = failed ? 1 : 0;
+      if (io.cand_terms) {  // the five running sums + terminal (without the q_0 terms)
+        double *ct = io.cand_terms + 6 * (size_t)m;
+        for (int a = 0; a < 5; ++a) ct[a] = sm[a];
+        ct[5] = S.cost[w];
+      }
     }
     const bool real = w < NWC && m < io.M;
     const unsigned nfm = __ballot_sync(kFull, real && !(c < dinf()));
@@ -1184,6 +1227,21 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
       tail_controls(io.rank_part, io.nominal, io.acc, P.H, P.nj, io.out);
       __syncthreads();
       VPB_TRACE(io, 2 * ncta + 11);
+      // One nonzero weight (the usual case at small lam): w = exp(0) = 1 and
+      // Z = 1, so U* = nominal + eps_best exactly and its re-evaluation is the
+      // best candidate's own evaluation -- reuse its sums.
+      const int single = (int)S.misc[45];
+      if (single >= 0 && io.rank_part[1] == 1.0) {
+        if (threadIdx.x < NWF) {
+          const double *ct = io.cand_terms + 6 * (size_t)single;
+          const int w = threadIdx.x;
+          for (int a = 0; a < 5; ++a) S.sums[w * 6 + a] = w == 0 ? __ldcg(ct + a) : 0.0;
+          S.cost[w] = w == 0 ? __ldcg(ct + 5) : 0.0;
+          S.fail[w] = 0;
+        }
+        __syncthreads();
+        break;
+      }
       state = 2;
     }
     VPB_TRACE(io, 2 * ncta + 12);
@@ -1563,7 +1621,7 @@ static AccLimit acc_of(const vpb_problem *p) {
 }
 
 struct SmpcWs {
-  double *cta_parts, *group_parts, *rank_part, *pro, *cand_costs;
+  double *cta_parts, *group_parts, *rank_part, *pro, *cand_costs, *cand_terms;
   unsigned int *counters;
   size_t bytes;
 };
@@ -1581,6 +1639,8 @@ static SmpcWs smpc_ws(void *base, int64_t M, int64_t H, int64_t n) {
   o += align_up((size_t)(2 * (M + 64) + ctas + 600) * 8, 256);
   w.cand_costs = reinterpret_cast<double *>(b + o);
   o += align_up((size_t)(M > 0 ? M : 1) * 8, 256);
+  w.cand_terms = reinterpret_cast<double *>(b + o);
+  o += align_up((size_t)(M > 0 ? M : 1) * 6 * 8, 256);
   w.rank_part = reinterpret_cast<double *>(b + o);
   o += align_up((size_t)L * 8, 256);
   w.pro = reinterpret_cast<double *>(b + o);
@@ -1680,6 +1740,7 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   io.rank_part = part_out ? part_out : w.rank_part;
   io.pro = w.pro;
   io.cand_costs = w.cand_costs;
+  io.cand_terms = w.cand_terms;
   io.finish = out != nullptr;
   io.out = out;
   io.acc = acc_of(prob);

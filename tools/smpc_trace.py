@@ -16,6 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--samples", type=int, default=4096)
     ap.add_argument("--horizon", type=int, default=32)
+    ap.add_argument("--flush", action="store_true", help="write 256 MiB before each traced launch (cold L2)")
     a = ap.parse_args()
     import bench
     from paper_2512_22575_b200 import _device as D
@@ -33,10 +34,13 @@ def main():
     torch.cuda.synchronize()
     lib = _lib.load()
     res = []
-    for _ in range(5):
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda") if a.flush else None
+    for it in range(5):
         buf.zero_()
+        if flush is not None:
+            flush.fill_(it)
         lib.vpb_debug_smpc_trace(D.ptr(buf))
-        pl.smpc_step_device(st, goal, field, nom, eps)
+        pl.smpc_generate_device(st, goal, field, nom, 3 + it)  # the production (fused-draw) step
         torch.cuda.synchronize()
         lib.vpb_debug_smpc_trace(None)
         t = buf.cpu().numpy().astype(np.float64)
