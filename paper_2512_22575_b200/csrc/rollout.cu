@@ -36,6 +36,7 @@ constexpr int NW = 8;                    // candidate warps per CTA (generic pat
 constexpr int NWF = 4;                   // candidate warps per CTA of the fixed-topology SMPC kernel
 constexpr int kThreads = (NW + 1) * 32;  // + terminal warp
 constexpr int kPartHead = 4;             // [m, Z, nonfinite, best_index]
+constexpr int kPartExt = 7;              // after N: [nonzero-weight count, the single candidate's 6 sums]
 constexpr int kGroup = 32;               // CTAs merged by a group's last CTA
 
 __device__ __forceinline__ void named_bar_sync(int id, int count) {
@@ -771,7 +772,7 @@ __device__ void merge_block(const Rows &R, int count, int hn, double lam, double
 
 // Rank records [m, Z, nf, best, N (hn)] as merge rows.
 __device__ __forceinline__ Rows record_rows(const double *rec, int hn) {
-  const int L = kPartHead + hn;
+  const int L = kPartHead + hn + kPartExt;
   return Rows{rec, rec + kPartHead, 1, L, L};
 }
 
@@ -1048,6 +1049,11 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
       dst[3] = (b0 >= 0 && b0 < ctas) ? heads[2 * (size_t)ctas + b0] : -1.0;
       misc[42] = (double)ncand;
       misc[45] = ncand == 1 ? (double)mlist[0] : -1.0;  // the only nonzero weight (U* = nominal + its eps)
+      // record extension: the nonzero count and that candidate's sums (lets a
+      // multi-device finish skip the re-evaluation too)
+      double *ext = dst + kPartHead + hn;
+      ext[0] = (double)ncand;
+      for (int a = 0; a < 6; ++a) ext[1 + a] = (ncand == 1 && io.cand_terms) ? __ldcg(io.cand_terms + 6 * (size_t)mlist[0] + a) : 0.0;
     }
   }
   __syncthreads();
@@ -1293,11 +1299,26 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), 1)
     smpc_tail_dyn<T, MAXJ>(P, D, merged, nominal, acc, out, S);
   } else {
     tail_controls(merged, nominal, acc, P.H, P.nj, out);
+    // one nonzero weight over all ranks (merged Z == 1, the minimum's rank has
+    // a single nonzero candidate): U* = nominal + eps_best, reuse its sums
+    const int hn = P.H * P.nj, Lr = kPartHead + hn + kPartExt;
+    int *short_row = reinterpret_cast<int *>(S.misc + 46);
+    if (threadIdx.x == 0) {
+      int r0 = -1, nz = 0;
+      for (int r = 0; r < n_parts; ++r) {
+        const double mr = parts[(size_t)r * Lr], zr = parts[(size_t)r * Lr + 1];
+        if (!(mr < dinf()) || zr * exp(-(mr - merged[0]) / lam) == 0.0) continue;
+        ++nz;
+        if (parts[(size_t)r * Lr + kPartHead + hn] == 1.0) r0 = r;
+      }
+      *short_row = (nz == 1 && merged[1] == 1.0) ? r0 : -1;
+    }
     __syncthreads();
+    const int srow = *short_row;
     const int warp = threadIdx.x >> 5;
-    // pass 0: U* split over the warps; pass 1: the q_0 prologue, split
+    // pass 0: U* split over the warps (skipped by the shortcut); pass 1: the q_0 prologue, split
 #pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
+    for (int pass = srow >= 0 ? 1 : 0; pass < 2; ++pass) {
       double *base = pass == 0 ? S.sums : S.scratch;
       fixed_candidate<T, double, Topo>(P, D, nullptr, pass == 0 ? out : nullptr, true, pass == 0 ? P.H : 1,
                                        pass == 0 ? 1 : 0, warp, NWF, base + warp * 6,
@@ -1322,6 +1343,12 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), 1)
       }
       S.cost[0] = c;
       S.fail[0] = f;
+      if (srow >= 0) {
+        const double *ext = parts + (size_t)srow * Lr + kPartHead + hn + 1;
+        for (int a = 0; a < 5; ++a) S.sums[a] = ext[a];
+        S.cost[0] = ext[5];
+        S.fail[0] = 0;
+      }
       S.pro[0] = pose0;
       S.pro[1] = coll0;
       *pro_fail(S) = bad;
@@ -1629,7 +1656,7 @@ struct SmpcWs {
 static SmpcWs smpc_ws(void *base, int64_t M, int64_t H, int64_t n) {
   const int64_t ctas = ceil_div(M > 0 ? M : 1, NWF);  // the larger CTA count of the two paths
   const int64_t groups = ceil_div(ctas, kGroup);
-  const int64_t L = kPartHead + H * n;
+  const int64_t L = kPartHead + H * n + kPartExt;
   SmpcWs w;
   char *b = reinterpret_cast<char *>(base);
   size_t o = 0;
@@ -1701,7 +1728,7 @@ int vpb_evaluate_batch(const vpb_problem *prob, const vpb_field *field, const vo
                                 : launch_rollout_t<float, double>(P, io, topo, s);
 }
 
-int64_t vpb_smpc_partial_len(int64_t H, int64_t n) { return kPartHead + H * n; }
+int64_t vpb_smpc_partial_len(int64_t H, int64_t n) { return kPartHead + H * n + kPartExt; }
 
 void vpb_debug_smpc_trace(unsigned long long *dev_buffer) { g_smpc_trace = dev_buffer; }
 
@@ -1844,7 +1871,7 @@ extern "C" {
 
 size_t vpb_smpc_finish_workspace_bytes(int64_t n_parts, int64_t H, int64_t n) {
   (void)n_parts;
-  return align_up((size_t)(kPartHead + H * n) * 8, 256) + 256;
+  return align_up((size_t)(kPartHead + H * n + kPartExt) * 8, 256) + 256;
 }
 
 int vpb_smpc_finish(const vpb_problem *prob, const vpb_field *field, const double *partials, int64_t n_parts,

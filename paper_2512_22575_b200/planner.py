@@ -629,6 +629,7 @@ class SmpcSession:
         self.h, self.n, self.m = p.horizon, planner.chain.dof, int(samples)
         L = load()
         self._lib = L
+        _release_pending_sessions()
         P = planner.problem(None, None)
         self._sigma = np.ascontiguousarray(np.broadcast_to(np.asarray(p.sigma, dtype=float), (self.n,)))
         handle = ctypes.c_void_p()
@@ -671,11 +672,28 @@ class SmpcSession:
         (device-side timing); the result is read by the next ``step``."""
         check(self._lib.vpb_smpc_session_launch(self._h, D.stream(self.pl.device)), "smpc_session_launch")
 
+    def close(self) -> None:
+        """Release the native session now (not during a stream capture)."""
+        h = getattr(self, "_h", None)
+        self._h = None
+        if h is not None and h.value:
+            check(self._lib.vpb_smpc_session_destroy(h), "smpc_session_destroy")
+
     def __del__(self):
+        # The garbage collector may run this while some stream is capturing a
+        # CUDA graph, where the cudaFree / cudaStreamDestroy of the native
+        # destroy would invalidate that capture: park the handle and release
+        # it at the next session creation instead.
         h = getattr(self, "_h", None)
         if h is not None and h.value:
-            try:
-                self._lib.vpb_smpc_session_destroy(h)
-            except Exception:  # interpreter shutdown
-                pass
+            _PENDING_DESTROY.append((self._lib, h))
             self._h = None
+
+
+_PENDING_DESTROY: list = []
+
+
+def _release_pending_sessions() -> None:
+    while _PENDING_DESTROY:
+        lib, h = _PENDING_DESTROY.pop()
+        lib.vpb_smpc_session_destroy(h)

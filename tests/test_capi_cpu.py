@@ -58,7 +58,7 @@ def test_pure_host_entry_points(lib):
     assert lib.vpb_version() == 1
     assert lib.vpb_occ_words(i64x3((4, 5, 33))) == 4 * 5 * 2
     assert lib.vpb_edt3d_workspace_bytes(i64x3((8, 8, 8))) >= 8 * 8 * 8 * 6
-    assert lib.vpb_smpc_partial_len(32, 7) == 4 + 224
+    assert lib.vpb_smpc_partial_len(32, 7) == 4 + 224 + 7
     assert lib.vpb_smpc_out_len(32, 7) == 2 * 224 + 7 + 13
 
 

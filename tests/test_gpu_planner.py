@@ -229,6 +229,39 @@ def test_smpc_step_vs_golden(pk, precision):
         np.testing.assert_allclose(res.diagnostics.e_ori, diag[3], rtol=1e-9, atol=1e-12)
 
 
+def test_finish_single_weight_shortcut_equals_reevaluation(pk):
+    """With one nonzero softmin weight over all ranks (tiny lambda) the
+    multi-device finish reuses that candidate's sums from its rank record
+    instead of re-evaluating U*; clearing the record's nonzero count forces
+    the re-evaluation, and both agree (vp/planner.py:373-400)."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.geometry import RigidTransform
+
+    chain, model = config.robot_7dof()
+    params = config.planner_params(7, {"samples": 1024, "horizon": 20, "lam": 1e-6})
+    pl = planner.Planner(chain, model, params, "fp32")
+    state = robot.JointState.resting(np.full(7, 0.1))
+    goal = RigidTransform.from_vec7([0.3, -0.2, 0.7, 0.9, 0.1, 0.3, -0.2])
+    nom = torch.from_numpy(0.1 * np.sin(np.arange(140)).reshape(20, 7)).cuda()
+    eps = pl.sample_device(5)
+    hn = 140
+    parts = []
+    for r in range(4):
+        p, _, _ = pl.smpc_partial_device(state, goal, None, nom, eps[r * 256:(r + 1) * 256].contiguous(),
+                                          m_offset=r * 256)
+        parts.append(p)
+    parts = torch.stack(parts)
+    assert int((parts[:, 4 + hn] == 1).sum()) >= 1
+    fast = pl.smpc_finish_device(state, goal, None, nom, parts).cpu().numpy()
+    slow_parts = parts.clone()
+    slow_parts[:, 4 + hn] = -1.0
+    slow = pl.smpc_finish_device(state, goal, None, nom, slow_parts).cpu().numpy()
+    np.testing.assert_array_equal(fast[:2 * hn + 7], slow[:2 * hn + 7])
+    np.testing.assert_allclose(fast, slow, rtol=1e-6, atol=1e-9, equal_nan=True)
+    single = pl.smpc_step_device(state, goal, None, nom, eps).cpu().numpy()
+    np.testing.assert_allclose(fast, single, rtol=1e-12, atol=1e-14, equal_nan=True)
+
+
 def test_smpc_shard_merge_equals_single(pk):
     """Sharded partials (2 and 8 shards of one batch) merged in rank order
     equal the single-device step."""
