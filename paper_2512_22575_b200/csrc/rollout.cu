@@ -828,19 +828,24 @@ __device__ __forceinline__ void tail_controls(const double *part, const double *
 // Diagnostics of the step (thread 0): re-evaluated cost of U* from slot 0 of
 // S (sums / cost / flags), best cost, Z, non-finite count, best index.
 __device__ __forceinline__ void tail_output(const Shared &S, const double *part, int H, int n, double best,
-                                            double nonfinite, double *out) {
-  if (threadIdx.x != 0) return;
+                                            double nonfinite, double *out, double *out_host = nullptr) {
   const int64_t base = 2 * (int64_t)H * n + n;
+  const int a = threadIdx.x;
+  if (a >= 13) return;
   const bool failed = S.fail[0] != 0 || S.tfail[0] != 0;
   const double *sm = S.sums;
-  out[base] = failed ? dinf() : sm[0] + sm[1] + sm[2] + sm[3] + sm[4] + S.cost[0];
-  for (int a = 0; a < 5; ++a) out[base + 1 + a] = failed ? 0.0 : sm[a];
-  out[base + 6] = failed ? 0.0 : S.cost[0];
-  out[base + 7] = best;
-  out[base + 8] = part[1];    // Z
-  out[base + 9] = nonfinite;  // non-finite sample count
-  out[base + 10] = part[3];   // best sample index
-  out[base + 11] = out[base + 12] = __longlong_as_double(0x7ff8000000000000ll);  // e_pos / e_ori: host
+  // slot a of [cost(U*), 5 sums, terminal, best, Z, non-finite, best index, e_pos, e_ori (host)]
+  double v;
+  if (a == 0) v = failed ? dinf() : sm[0] + sm[1] + sm[2] + sm[3] + sm[4] + S.cost[0];
+  else if (a < 6) v = failed ? 0.0 : sm[a - 1];
+  else if (a == 6) v = failed ? 0.0 : S.cost[0];
+  else if (a == 7) v = best;
+  else if (a == 8) v = part[1];
+  else if (a == 9) v = nonfinite;
+  else if (a == 10) v = part[3];
+  else v = __longlong_as_double(0x7ff8000000000000ll);
+  out[base + a] = v;
+  if (out_host) out_host[base + a] = v;
 }
 
 // Generic path tail: U*, then its M = 1 re-evaluation on warps 0 and NW.
@@ -875,9 +880,13 @@ __device__ __forceinline__ void fixed_shard_fixup(const Shared &S, int64_t M, do
                                                   double *part) {
   const bool bad = *pro_fail(S) != 0;
   const double add = S.pro[0] + S.pro[1];
-  for (int64_t m = threadIdx.x; m < M; m += blockDim.x) {
-    if (costs) costs[m] = bad ? dinf() : costs[m] + add;
-    if (flags && bad) flags[m] = 1;
+  // (kept rolled: this runs once per step on a cold instruction cache)
+  if (costs || (flags && bad)) {
+#pragma unroll 1
+    for (int64_t m = threadIdx.x; m < M; m += blockDim.x) {
+      if (costs) costs[m] = bad ? dinf() : costs[m] + add;
+      if (flags && bad) flags[m] = 1;
+    }
   }
   if (threadIdx.x == 0 && part) {
     part[0] = bad ? dinf() : part[0] + add;
@@ -885,25 +894,47 @@ __device__ __forceinline__ void fixed_shard_fixup(const Shared &S, int64_t M, do
   }
 }
 
-// Per-candidate totals -> CTA softmin partial -> group merge by the group's
-// last CTA -> global merge by the last group into io.rank_part.  Returns
-// true on the CTA that did the global merge (all others are done).
+// Shared-memory slots of the final merge and the fixed-path tail (S.scratch,
+// kMergeScratch doubles): the merge keeps what the tail needs on chip so the
+// last CTA's chain of dependent global round trips stays short.
+constexpr int kMergeScratch = 64;  // smem_layout scratch argument of smpc_kernel
+constexpr int kFmW = 0;            // [32] weights of the first nonzero candidates
+constexpr int kFmCT = 32;          // [6] sums of the minimum's candidate (speculative, for the shortcut)
+constexpr int kFmRec = 40;         // [4] the shard record head: min, Z, non-finite, best index
+constexpr int kFmBest = 44;        // local index of the minimum's candidate
+constexpr int kFmCL = 48;          // ints: [nw][kFmCap] nonzero CTAs per warp
+constexpr int kFmML = 120;         // ints: [32] indices of the first nonzero candidates
+constexpr int kFmWN = 136;         // ints: [nw] nonzero CTA count per warp
+constexpr int kFmCap = 16;
+
 // Final merge of the single-device step, by the last CTA.  Inputs: the CTA
 // heads (structure-of-arrays [3][ctas]: min cost, non-finite count, best
 // global index) and every candidate's cost.  Output: the shard record
-// [min, Z, non-finite, best, N (hn)] with weights w_m = exp(-(S_m - min)/lam)
-// in candidate order.  A CTA whose own minimum is far above the global one
+// [min, Z, non-finite, best, N (hn), ext] with weights
+// w_m = exp(-(S_m - min)/lam) in candidate order (io.rank_part, and the head
+// in smem at kFmRec).  A CTA whose own minimum is far above the global one
 // (exp underflow) contributes exactly zero and is skipped before any of its
-// candidates is touched; at the planner's lam almost all are.
-template <typename ET, int NWC>
+// candidates is touched; at the planner's lam almost all are.  Lists live in
+// global scratch with their first entries mirrored in smem.  FIXED: while
+// warp 0 expands the candidates, warp 1 fetches the minimum's sums (the
+// single-weight shortcut) and warp 2 the q_0 prologue terms of block 0.
+// `fused_u` (fixed path, finishing): U*, the clipped command and the shifted
+// warm start are produced in the N pass itself (to out and out_host).
+template <typename ET, int NWC, bool FIXED>
 __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *heads, const double *costs, int ctas,
-                            int hn, unsigned long long *trace_head) {
+                            int hn, int nj, bool fused_u, unsigned long long *trace_head) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   double *misc = S.misc;
-  double *wlist = io.group_parts;                                  // candidate weights (scratch)
+  double *sc = S.scratch;
+  double *wlist = io.group_parts;                                  // candidate weights
   int *mlist = reinterpret_cast<int *>(io.group_parts + io.M + 64);  // candidate indices
   int *clist = reinterpret_cast<int *>(io.group_parts + io.M + 64) + io.M + 64;  // nonzero CTAs, per-warp slices
+  int *sclist = reinterpret_cast<int *>(sc + kFmCL);
+  int *smlist = reinterpret_cast<int *>(sc + kFmML);
   const double inv_lam = 1.0 / io.lam;
+  if (fused_u) {  // the nominal is read by the U* pass at the end: start it towards L2 now
+    for (int e = tid * 16; e < hn; e += nt * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(io.nominal + e));
+  }
   // 1. global minimum over the CTA heads (first CTA attaining it)
   constexpr int kHR = 8;  // heads kept in registers per lane (ctas <= nw * 32 * kHR)
   const int span = ((ctas + nw - 1) / nw + 31) & ~31;
@@ -930,6 +961,7 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
       }
     }
   } else {
+#pragma unroll 1
     for (int c = w0; c < w1; c += 32 * 4) {
       double v[4], f[4];
 #pragma unroll
@@ -958,63 +990,72 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
     }
   }
   nf = warp_sum_d(nf);
+  if (trace_head && tid == 0) trace_head[1] = gtimer();
   if (lane == 0) {
     misc[warp] = mn;
     misc[16 + warp] = (double)bidx;
     misc[32 + warp] = nf;
   }
   __syncthreads();
-  if (tid == 0) {
-    double m0 = dinf(), NF = 0.0;
-    int b0 = 0x7fffffff;
-    for (int w = 0; w < nw; ++w) {
-      const double v = misc[w];
-      const int b = (int)misc[16 + w];
-      NF += misc[32 + w];
-      if (v < m0 || (v == m0 && b < b0)) {
-        m0 = v;
-        b0 = b;
-      }
+  // every thread combines the warp results (fixed warp order)
+  double m0 = dinf(), NF = 0.0;
+  int b0 = 0x7fffffff;
+#pragma unroll 1
+  for (int w = 0; w < nw; ++w) {
+    const double v = misc[w];
+    const int b = (int)misc[16 + w];
+    NF += misc[32 + w];
+    if (v < m0 || (v == m0 && b < b0)) {
+      m0 = v;
+      b0 = b;
     }
-    misc[40] = m0;
-    misc[41] = (double)b0;
-    misc[43] = NF;
   }
-  __syncthreads();
-  const double m0 = misc[40];
+  if (trace_head && tid == 0) trace_head[2] = gtimer();
   // 2. (all warps) CTAs with a nonzero weight, compacted in order into this
-  //    warp's slice of clist (cheap exponent pre-check; exp only near the min)
+  //    warp's slice of clist (+ its first kFmCap in smem); exp-free,
+  //    conservative test (exp(-x) underflows to 0 for x > 745.14; the
+  //    expansion below computes the exact weights)
   int wn = 0;
   auto consider = [&](int i, double v) {
-    const double x = (v - m0) * inv_lam;
-    const bool nz = v < dinf() && x < 746.0 && exp(-x) != 0.0;
+    const bool nz = v < dinf() && (v - m0) * inv_lam < 746.0;
     const unsigned bal = __ballot_sync(kFull, nz);
-    if (nz) clist[w0 + wn + __popc(bal & ((1u << lane) - 1u))] = i;
+    if (nz) {
+      const int p = wn + __popc(bal & ((1u << lane) - 1u));
+      clist[w0 + p] = i;
+      if (p < kFmCap) sclist[warp * kFmCap + p] = i;
+    }
     wn += __popc(bal);
   };
   if (in_regs) {
 #pragma unroll
     for (int t = 0; t < kHR; ++t) consider(w0 + 32 * t + lane, hv[t]);
   } else {
+#pragma unroll 1
     for (int c = w0; c < w1; c += 32) {
       const int i = c + lane;
       consider(i, i < w1 ? heads[i] : dinf());
     }
   }
-  if (lane == 0) misc[16 + warp] = (double)wn;
+  int *wcount = reinterpret_cast<int *>(sc + kFmWN);
+  if (lane == 0) wcount[warp] = wn;
   __syncthreads();
+  if (trace_head && tid == 0) trace_head[3] = gtimer();
+  const int b0c = (b0 >= 0 && b0 < ctas) ? b0 : 0;
   if (tid < 32) {
-    // 3. (warp 0) the candidates of those CTAs, in order: weights and Z
-    // candidates of the nonzero CTAs over the concatenated warp slices, 32
-    // at a time: one load round trip per 32 candidates
+    // 3. (warp 0) the candidates of those CTAs, in order: weights and Z,
+    //    32 candidates per load round trip
     int off[16];
     int total = 0;
+    bool small = true;
     for (int w = 0; w < nw; ++w) {
       off[w] = total;
-      total += (int)misc[16 + w] * NWC;
+      const int c = wcount[w];
+      small = small && c <= kFmCap;
+      total += c * NWC;
     }
     int ncand = 0;
     double z = 0.0;
+#pragma unroll 1
     for (int k0 = 0; k0 < total; k0 += 32) {
       const int k = k0 + lane;
       int m = -1;
@@ -1024,7 +1065,8 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
         for (int u = 1; u < nw; ++u)
           if (k >= off[u]) w = u;
         const int r = k - off[w];
-        m = clist[w * span + r / NWC] * NWC + (r % NWC);
+        const int ci = small ? sclist[w * kFmCap + r / NWC] : clist[w * span + r / NWC];
+        m = ci * NWC + (r % NWC);
         if (m < io.M) {
           const double c = costs[m];
           wt = c < dinf() ? exp(-(c - m0) * inv_lam) : 0.0;
@@ -1035,44 +1077,114 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
         const int p = ncand + __popc(bal & ((1u << lane) - 1u));
         mlist[p] = m;
         wlist[p] = wt;
+        if (p < 32) {
+          smlist[p] = m;
+          sc[kFmW + p] = wt;
+        }
       }
       z += wt;  // lane-strided partials in candidate order
       ncand += __popc(bal);
     }
     z = warp_sum_d(z);
     if (lane == 0) {
-      const int b0 = (int)misc[41];
       double *dst = io.rank_part;
       dst[0] = m0;
       dst[1] = z;
-      dst[2] = misc[43];
-      dst[3] = (b0 >= 0 && b0 < ctas) ? heads[2 * (size_t)ctas + b0] : -1.0;
+      dst[2] = NF;
+      sc[kFmRec + 0] = m0;
+      sc[kFmRec + 1] = z;
+      sc[kFmRec + 2] = NF;
       misc[42] = (double)ncand;
-      misc[45] = ncand == 1 ? (double)mlist[0] : -1.0;  // the only nonzero weight (U* = nominal + its eps)
-      // record extension: the nonzero count and that candidate's sums (lets a
-      // multi-device finish skip the re-evaluation too)
-      double *ext = dst + kPartHead + hn;
-      ext[0] = (double)ncand;
-      for (int a = 0; a < 6; ++a) ext[1 + a] = (ncand == 1 && io.cand_terms) ? __ldcg(io.cand_terms + 6 * (size_t)mlist[0] + a) : 0.0;
+      misc[45] = ncand == 1 ? (double)smlist[0] : -1.0;  // the only nonzero weight (U* = nominal + its eps)
+      if (trace_head) trace_head[4] = gtimer();
+    }
+  } else if (warp == 1) {
+    // the minimum's global index, and (fixed path) its candidate's sums: when
+    // it is the only nonzero weight, they are the re-evaluation of U*
+    const double bg = b0 < ctas ? heads[2 * (size_t)ctas + b0c] : -1.0;
+    const int bl = bg >= 0.0 ? (int)(bg - (double)io.m_offset) : -1;
+    if (FIXED && io.cand_terms && lane < 6 && bl >= 0) sc[kFmCT + lane] = __ldcg(io.cand_terms + 6 * (size_t)bl + lane);
+    if (lane == 0) {
+      sc[kFmRec + 3] = bg;
+      sc[kFmBest] = (double)bl;
+    }
+    if (trace_head && lane == 0) trace_head[5] = gtimer();
+  } else if (FIXED && warp == 2) {
+    // block 0's q_0 prologue terms (normally long done), summed in split order
+    unsigned int *pro_ready = io.counters + (ctas + kGroup - 1) / kGroup + 1;
+    if (lane == 0) {
+      while (ld_acquire_gpu(pro_ready) == 0u) __nanosleep(64);
+      *pro_ready = 0u;  // counters return to zero for the next launch
+    }
+    __syncwarp();
+    const bool has = lane < NWF;
+    const double pw = has ? __ldcg(io.pro + 4 * lane + 0) : 0.0;
+    const double cw = has ? __ldcg(io.pro + 4 * lane + 1) : 0.0;
+    const unsigned badm = __ballot_sync(kFull, has && __ldcg(io.pro + 4 * lane + 2) != 0.0);
+    const double pose0 = warp_sum_d(pw), coll0 = warp_sum_d(cw);
+    if (lane == 0) {
+      S.pro[0] = pose0;
+      S.pro[1] = coll0;
+      *pro_fail(S) = badm != 0u;
+      if (trace_head) trace_head[6] = gtimer();
     }
   }
   __syncthreads();
   if (trace_head && tid == 0) *trace_head = gtimer();
-  // 3. N = sum_m w_m eps_m over the nonzero candidates, in candidate order
   const int ncand = (int)misc[42];
+  if (tid == 32) {
+    // record tail: best index and the extension [nonzero count, the single
+    // candidate's 6 sums] (lets a multi-device finish skip the re-evaluation)
+    double *dst = io.rank_part;
+    dst[3] = sc[kFmRec + 3];
+    double *ext = dst + kPartHead + hn;
+    const bool one = ncand == 1 && io.cand_terms && (int)sc[kFmBest] == smlist[0];
+    ext[0] = (FIXED && io.cand_terms) ? (double)ncand : -1.0;
+    for (int a = 0; a < 6; ++a) ext[1 + a] = one ? sc[kFmCT + a] : 0.0;
+  }
+  // 4. N = sum_m w_m eps_m over the nonzero candidates, in candidate order
+  //    (+ U* = nominal + N / Z, clipped command, shifted warm start)
   const ET *eps = reinterpret_cast<const ET *>(io.eps);
+  const bool sl = ncand <= 32;
+  const int *ml = sl ? smlist : mlist;
+  const double *wl = sl ? sc + kFmW : wlist;
+  const double Z = sc[kFmRec + 1];
+#pragma unroll 1
   for (int e = tid; e < hn; e += nt) {
     double acc = 0.0;
     int k = 0;
+#pragma unroll 1
     for (; k + 4 <= ncand; k += 4) {
       double a[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = load_e<ET>(eps + (size_t)mlist[k + t] * hn + e);
+      for (int t = 0; t < 4; ++t) a[t] = load_e<ET>(eps + (size_t)ml[k + t] * hn + e);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) acc += wlist[k + t] * a[t];
+      for (int t = 0; t < 4; ++t) acc += wl[k + t] * a[t];
     }
-    for (; k < ncand; ++k) acc += wlist[k] * load_e<ET>(eps + (size_t)mlist[k] * hn + e);
+#pragma unroll 1
+    for (; k < ncand; ++k) acc += wl[k] * load_e<ET>(eps + (size_t)ml[k] * hn + e);
     io.rank_part[kPartHead + e] = acc;
+    if (fused_u) {  // tail_controls, element e
+      const double u = io.nominal[e] + acc / Z;
+      const int64_t o2 = (int64_t)hn + e;  // clipped command (e < nj) / shifted warm start
+      double v2 = u;
+      if (e < nj) {
+        const double lim = io.acc.v[e];
+        v2 = u < -lim ? -lim : (u > lim ? lim : u);
+      }
+      io.out[e] = u;
+      io.out[o2] = v2;
+      if (io.out_host) {
+        io.out_host[e] = u;
+        io.out_host[o2] = v2;
+      }
+    }
+  }
+  if (fused_u) {
+    for (int e = tid; e < nj; e += nt) {
+      io.out[2 * (int64_t)hn + e] = 0.0;
+      if (io.out_host) io.out_host[2 * (int64_t)hn + e] = 0.0;
+    }
   }
   __syncthreads();
 }
@@ -1080,8 +1192,9 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
 // Per-CTA head (warp 0: min cost, non-finite count, best index of the CTA's
 // candidates; costs to `costs`), publication, and -- on the last CTA -- the
 // final merge.  Returns true on the CTA that merged.
-template <typename ET, int NWC>
-__device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t cta_m0, int hn, int cta, int ctas) {
+template <typename ET, int NWC, bool FIXED>
+__device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t cta_m0, int hn, int nj, int cta,
+                                     int ctas) {
   const int groups = (ctas + kGroup - 1) / kGroup;
   double *heads = io.cta_parts;  // [3][ctas]
   double *costs = io.costs ? io.costs : io.cand_costs;
@@ -1132,7 +1245,8 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
   VPB_TRACE(io, 2 * ctas + 3 + (cta % 4));
   if (flag[0] == 0u) return false;
   VPB_TRACE(io, 2 * ctas);
-  final_merge<ET, NWC>(io, S, heads, costs, ctas, hn, io.trace ? io.trace + 2 * ctas + 13 : nullptr);
+  final_merge<ET, NWC, FIXED>(io, S, heads, costs, ctas, hn, nj, FIXED && io.finish,
+                              io.trace ? io.trace + 2 * ctas + 13 : nullptr);
   if (threadIdx.x == 0) io.counters[groups] = 0u;
   VPB_TRACE(io, 2 * ctas + 1);
   return true;
@@ -1144,7 +1258,7 @@ template <typename T, typename ET, int MAXJ, typename Topo>
 __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>())
     smpc_kernel(const __grid_constant__ Prob<T> P, const __grid_constant__ SmpcIO io) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const SmemLayout L = smem_layout(is_dyn_v<Topo> ? P.ns : 0, sizeof(T), 0);
+  const SmemLayout L = smem_layout(is_dyn_v<Topo> ? P.ns : 0, sizeof(T), kMergeScratch);
   const Shared S = carve(smem_raw, L);
   Dyn<T> &D = *reinterpret_cast<Dyn<T> *>(S.dyn);
   if (threadIdx.x < 32) load_dyn<T>(P, io.dyn, D);
@@ -1156,7 +1270,7 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
     VPB_TRACE(io, 2 * blockIdx.x);
     CandOut co{nullptr, nullptr, nullptr};
     evaluate_cta<T, ET, MAXJ>(P, D, eps, io.nominal, io.M, cta_m0, S, co);
-    if (!cta_reduce_and_merge<ET, smpc_nw<Topo>()>(io, S, cta_m0, hn, blockIdx.x, gridDim.x)) return;
+    if (!cta_reduce_and_merge<ET, smpc_nw<Topo>(), false>(io, S, cta_m0, hn, P.nj, blockIdx.x, gridDim.x)) return;
     if (io.finish) {
       smpc_tail_dyn<T, MAXJ>(P, D, io.rank_part, io.nominal, io.acc, io.out, S);
       if (io.out_host) {
@@ -1206,43 +1320,26 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
       S.tfail[warp] = 0;
       __syncthreads();
       VPB_TRACE(io, 2 * cta + 1);
-      if (!cta_reduce_and_merge<ET, smpc_nw<Topo>()>(io, S, cm0, hn, cta, ncta)) return;
-      if (threadIdx.x == 0) {  // wait for the prologue block (normally long done)
-        while (ld_acquire_gpu(pro_ready) == 0u) __nanosleep(64);
-        *pro_ready = 0u;  // counters return to zero for the next launch
-      }
-      __syncthreads();
-      if (threadIdx.x < 32) {  // q_0 terms, summed in fixed split order
-        const int w = threadIdx.x;
-        const bool has = w < NWF;
-        const double pw = has ? __ldcg(io.pro + 4 * w + 0) : 0.0;
-        const double cw = has ? __ldcg(io.pro + 4 * w + 1) : 0.0;
-        const unsigned badm = __ballot_sync(kFull, has && __ldcg(io.pro + 4 * w + 2) != 0.0);
-        const double pose0 = warp_sum_d(pw), coll0 = warp_sum_d(cw);
-        if (w == 0) {
-          S.pro[0] = pose0;
-          S.pro[1] = coll0;
-          *pro_fail(S) = badm != 0u;
-        }
-      }
+      // (the final merge also fetched the q_0 terms into S.pro and, when
+      // finishing, wrote U*, the command and the warm start)
+      if (!cta_reduce_and_merge<ET, smpc_nw<Topo>(), true>(io, S, cm0, hn, P.nj, cta, ncta)) return;
       if (!io.finish) {
-        __syncthreads();
         fixed_shard_fixup(S, io.M, io.costs, io.flags, io.rank_part);
         return;
       }
-      tail_controls(io.rank_part, io.nominal, io.acc, P.H, P.nj, io.out);
-      __syncthreads();
       VPB_TRACE(io, 2 * ncta + 11);
       // One nonzero weight (the usual case at small lam): w = exp(0) = 1 and
       // Z = 1, so U* = nominal + eps_best exactly and its re-evaluation is the
-      // best candidate's own evaluation -- reuse its sums.
+      // best candidate's own evaluation -- reuse its sums (fetched by the
+      // merge when that candidate is the minimum's, as it must be).
       const int single = (int)S.misc[45];
-      if (single >= 0 && io.rank_part[1] == 1.0) {
+      if (single >= 0 && S.scratch[kFmRec + 1] == 1.0) {
         if (threadIdx.x < NWF) {
+          const bool spec = (int)S.scratch[kFmBest] == single;
           const double *ct = io.cand_terms + 6 * (size_t)single;
           const int w = threadIdx.x;
-          for (int a = 0; a < 5; ++a) S.sums[w * 6 + a] = w == 0 ? __ldcg(ct + a) : 0.0;
-          S.cost[w] = w == 0 ? __ldcg(ct + 5) : 0.0;
+          for (int a = 0; a < 5; ++a) S.sums[w * 6 + a] = w == 0 ? (spec ? S.scratch[kFmCT + a] : __ldcg(ct + a)) : 0.0;
+          S.cost[w] = w == 0 ? (spec ? S.scratch[kFmCT + 5] : __ldcg(ct + 5)) : 0.0;
           S.fail[w] = 0;
         }
         __syncthreads();
@@ -1270,14 +1367,11 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
     }
     __syncthreads();
     const bool bad = *pro_fail(S) != 0;
-    const double best = bad ? dinf() : io.rank_part[0] + S.pro[0] + S.pro[1];
-    tail_output(S, io.rank_part, P.H, P.nj, best, bad ? (double)io.M : io.rank_part[2], io.out);
+    const double *rec = S.scratch + kFmRec;
+    const double best = bad ? dinf() : rec[0] + S.pro[0] + S.pro[1];
+    // (out_host: zero-copy result, posted PCIe writes visible after the kernel completes)
+    tail_output(S, rec, P.H, P.nj, best, bad ? (double)io.M : rec[2], io.out, io.out_host);
     fixed_shard_fixup(S, io.M, io.costs, io.flags, nullptr);
-    if (io.out_host) {  // zero-copy result: posted PCIe writes, visible after the kernel completes
-      __syncthreads();
-      const int len = 2 * P.H * P.nj + P.nj + 13;
-      for (int e = threadIdx.x; e < len; e += blockDim.x) io.out_host[e] = io.out[e];
-    }
     VPB_TRACE(io, 2 * ncta + 2);
   }
 }
@@ -1601,7 +1695,7 @@ template <typename T, typename ET>
 static int launch_smpc_t(const Prob<T> &P, const SmpcIO &io, int topo, cudaStream_t s) {
   const int64_t ctas = ceil_div(io.M, topo ? NWF : NW) + (topo ? 1 : 0);  // fixed path: + prologue block
   const int groups = (int)ceil_div(ctas, kGroup);
-  const size_t smem = smem_bytes(P, 0, topo);
+  const size_t smem = smem_bytes(P, kMergeScratch, topo);
   int rc;
   if (topo == 1) {
     auto k = smpc_kernel<T, ET, 8, TopoRobot7>;
