@@ -316,20 +316,33 @@ __device__ __forceinline__ bool fixed_config(const Prob<T> &P, const FixedConsts
   // self pairs (vp/batch.py:294-302): squared pre-check, sqrt only on contact
   T self = T(0);
   if (spheres) {
+    // fast pass: a pair can touch only if d^2 < rsum2 (a conservative bound
+    // of (r_i + r_j)^2); the exact penalties are summed only on lanes where
+    // some pair may touch (rare), in the same pair order as always
+    bool touch = false;
     static_for<0, NP>([&](auto pc) {
       constexpr int p = decltype(pc)::value;
       constexpr int i = Topo::pair_i(p), j = Topo::pair_j(p);
       const T dx = cx[i] - cx[j], dy = cy[i] - cy[j], dz = cz[i] - cz[j];
       const T d2 = dx * dx + dy * dy + dz * dz;
-      T gap;
-      if constexpr (sizeof(T) == 8) {
-        gap = sqrt(d2) - C.rsum[p];
-      } else {
-        gap = d2 * rsqrtf(fmaxf(d2, 1e-30f)) - C.rsum[p];
-      }
-      const T pen = gap < T(0) ? P.w_self * gap * gap : T(0);
-      self += ((W.pmask >> p) & 1ull) ? pen : T(0);
+      touch |= d2 < C.rsum2[p] && ((W.pmask >> p) & 1ull);
     });
+    if (touch) {
+      static_for<0, NP>([&](auto pc) {
+        constexpr int p = decltype(pc)::value;
+        constexpr int i = Topo::pair_i(p), j = Topo::pair_j(p);
+        const T dx = cx[i] - cx[j], dy = cy[i] - cy[j], dz = cz[i] - cz[j];
+        const T d2 = dx * dx + dy * dy + dz * dz;
+        T gap;
+        if constexpr (sizeof(T) == 8) {
+          gap = sqrt(d2) - C.rsum[p];
+        } else {
+          gap = d2 * rsqrtf(fmaxf(d2, 1e-30f)) - C.rsum[p];
+        }
+        const T pen = gap < T(0) ? P.w_self * gap * gap : T(0);
+        self += ((W.pmask >> p) & 1ull) ? pen : T(0);
+      });
+    }
   }
   coll = env + self;
   return ok;
