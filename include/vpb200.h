@@ -123,7 +123,9 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3],
               void *workspace, size_t workspace_bytes, void *stream);
 
 /* Distance field view (vp/mapping.py:556-583, DistanceField) consumed by the
- * query and by the rollout kernel. */
+ * query and by the rollout kernel.  `sq` holds exact squared voxel distances
+ * between voxel centres (+inf = no source), as vpb_edt3d writes them: the
+ * fp32 rollout relies on sqrt(sq) being 1-Lipschitz to skip far cells. */
 typedef struct {
   const float *sq; /* (dev) (n0, n1, n2), NULL = no field (snap=None) */
   int64_t n[3];

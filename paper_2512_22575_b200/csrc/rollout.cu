@@ -1583,6 +1583,8 @@ static int build_prob(const vpb_problem *p, const vpb_field *f, Prob<T> &P) {
     C.dr[s] = (T)dr;
     const double t = dr / vox;
     C.thr2[s] = (T)(t * t * (1.0 + 1e-4) + 1e-12);
+    const double tf = t + 1.7320508075688772 + 0.01;  // + the cell diagonal + rounding margin (voxels)
+    C.far2[s] = (T)(tf * tf);
     C.zero_cost[s] = (T)(p->w_env * (p->d_act - (0.0 - r)) * (p->d_act - (0.0 - r)));
     const double go = p->d_act - (outside - r);
     C.out_cost[s] = (T)(go > 0.0 ? p->w_env * go * go : 0.0);

@@ -20,6 +20,7 @@ template <typename T>
 struct FixedConsts {
   T dr[kMaxS];         // d_act + r_s
   T thr2[kMaxS];       // squared-voxel value above which the env term is certainly 0
+  T far2[kMaxS];       // corner value above which every corner of the cell is beyond thr (see env_cost)
   T zero_cost[kMaxS];  // env cost when the containing cell is occupied (distance 0)
   T out_cost[kMaxS];   // env cost outside the field volume
   T rsum[kMaxP];       // r_i + r_j

@@ -141,7 +141,11 @@ __device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C,
     g2 = (pz - P.origin2) * P.inv_voxel - P.lo2;
   }
   const bool inside = g0 >= T(0) && g0 < C.nf0 && g1 >= T(0) && g1 < C.nf1 && g2 >= T(0) && g2 < C.nf2;
-  if (!inside) g0 = g1 = g2 = T(0);  // any in-range address; the result is selected away
+  if constexpr (sizeof(T) == 4) {
+    if (!inside) return C.out_cost[s];
+  } else {
+    if (!inside) g0 = g1 = g2 = T(0);  // any in-range address; the result is selected away
+  }
   // c = g - 1/2 clamped to [0, n - 1] (vp/mapping.py:654-663)
   T c0 = g0 - T(0.5), c1 = g1 - T(0.5), c2 = g2 - T(0.5);
   c0 = fmin(fmax(c0, T(0)), C.chi0);
@@ -151,7 +155,17 @@ __device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C,
   const T f0 = c0 - a0, f1 = c1 - a1, f2 = c2 - a2;  // in [0, 1]
   const int i0 = (int)a0, i1 = (int)a1, i2 = (int)a2;
   const float *p = sq + ((i0 * P.n1 + i1) * P.n2 + i2);
-  const float v0 = __ldg(p), v1 = __ldg(p + C.off2);
+  const float v0 = __ldg(p);
+  if constexpr (sizeof(T) == 4) {
+    // Far-field exit: the field holds exact squared distances between voxel
+    // centres (vpb_edt3d), so sqrt(field) is 1-Lipschitz and every corner of
+    // the cell has sqrt(v) >= sqrt(v0) - sqrt(3); the interpolated distance is
+    // then beyond d_act + r and the term is exactly 0 (the containing cell is
+    // not occupied either).  Most spheres of most steps leave here after one
+    // load instead of eight.
+    if (v0 >= C.far2[s]) return T(0);
+  }
+  const float v1 = __ldg(p + C.off2);
   const float *py_ = p + C.off1;
   const float v2 = __ldg(py_), v3 = __ldg(py_ + C.off2);
   const float *px_ = p + C.off0;

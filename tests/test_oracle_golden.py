@@ -157,3 +157,24 @@ def test_softmin_validation_errors():
         oracle.soft_weights(np.array([1.0, np.inf]), 0.5)
     with pytest.raises(ValueError):
         oracle.soft_weights(np.array([1.0]), 0.0)
+
+
+def test_golden_fields_are_lipschitz_edts():
+    """The fp32 rollout's far-cell exit (rollout_fixed.cuh, env_cost) assumes
+    sqrt(field) is 1-Lipschitz between voxel centres, which holds for an
+    exact EDT.  Pin it on every field the reference produced."""
+    g = load_golden("rollout")
+    i = 0
+    checked = 0
+    while f"r_field_sq_{i}" in g:
+        d = np.sqrt(i32_to_sq(g[f"r_field_sq_{i}"]))
+        if np.isfinite(d).all():
+            for sh in [(1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 0), (1, 0, 1), (0, 1, 1), (1, 1, 1)]:
+                a = d[:d.shape[0] - sh[0], :d.shape[1] - sh[1], :d.shape[2] - sh[2]]
+                b = d[sh[0]:, sh[1]:, sh[2]:]
+                assert np.abs(a - b).max() <= np.sqrt(sum(sh)) + 1e-9
+            checked += 1
+        else:
+            assert np.isinf(d).all()  # no source at all
+        i += 1
+    assert checked >= 1
