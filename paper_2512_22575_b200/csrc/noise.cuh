@@ -102,11 +102,11 @@ __device__ __forceinline__ void candidate_noise(const NoiseGen &G, int64_t m_loc
   }
   const int lo = max(0, k - back), hi = min(H, k + fwd + 1);
   const float scale = (mg == 0 || k >= H) ? 0.0f : rsqrtf((float)(hi - lo));
-  // window offsets d in use at this step (bit d + HALF), computed once
-  unsigned dmask = 0u;
+  // window offsets d in use at this step, computed once
+  float dm[2 * HALF + 1];  // 1 / 0 per window offset
 #pragma unroll
   for (int d = -HALF; d <= HALF; ++d)
-    if (d >= -back && d <= fwd && k + d >= 0 && k + d < H) dmask |= 1u << (d + HALF);
+    dm[d + HALF] = (d >= -back && d <= fwd && k + d >= 0 && k + d < H) ? 1.0f : 0.0f;
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     float acc = 0.0f;
@@ -118,7 +118,7 @@ __device__ __forceinline__ void candidate_noise(const NoiseGen &G, int64_t m_loc
         const float vh = __shfl_sync(kFull, zh[j], src < 0 ? src + 4 : (src - 28) & 31);
         v = (src < 0 || src >= 32) ? vh : v;
       }
-      acc += ((dmask >> (d + HALF)) & 1u) ? v : 0.0f;
+      acc = fmaf(dm[d + HALF], v, acc);  // == acc + (in window ? v : 0), v finite
     }
     u[j] = acc * scale * G.sigma[j];
   }

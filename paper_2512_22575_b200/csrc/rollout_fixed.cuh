@@ -127,76 +127,95 @@ __device__ __forceinline__ void fixed_link(const Prob<T> &P, T q, T R[9], T t[3]
 // to n - 2 so the eight corners are base + {0, off0} + {0, off1} + {0, off2}
 // (the reference's b = min(a + 1, n - 1) gives the same value: at the upper
 // border its weight on b is 0 and ours puts weight 1 on the same voxel).
-template <typename T>
-__device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C, const float *sq, int s, T px, T py,
-                                      T pz) {
-  T g0, g1, g2;
-  if constexpr (sizeof(T) == 8) {
-    g0 = (px - P.origin0) / P.voxel - P.lo0;
-    g1 = (py - P.origin1) / P.voxel - P.lo1;
-    g2 = (pz - P.origin2) / P.voxel - P.lo2;
-  } else {
-    g0 = (px - P.origin0) * P.inv_voxel - P.lo0;
-    g1 = (py - P.origin1) * P.inv_voxel - P.lo1;
-    g2 = (pz - P.origin2) * P.inv_voxel - P.lo2;
-  }
-  const bool inside = g0 >= T(0) && g0 < C.nf0 && g1 >= T(0) && g1 < C.nf1 && g2 >= T(0) && g2 < C.nf2;
-  if constexpr (sizeof(T) == 4) {
-    if (!inside) return C.out_cost[s];
-  } else {
-    if (!inside) g0 = g1 = g2 = T(0);  // any in-range address; the result is selected away
-  }
+//
+// fp32 (production): the containing cell floor(g) is loaded first.  The field
+// holds exact squared distances between voxel centres (vpb_edt3d), so
+// sqrt(field) is 1-Lipschitz and every interpolation corner -- the cell is one
+// of them -- has sqrt(v) >= sqrt(cell) - sqrt(3); past C.far2 the interpolated
+// distance is beyond d_act + r and the term is exactly 0.  Most spheres of
+// most steps leave after that one load.
+__device__ __forceinline__ float env_cost_f32(const Prob<float> &P, const FixedConsts<float> &C, const float *sq,
+                                              int s, float px, float py, float pz) {
+  const float g0 = (px - P.origin0) * P.inv_voxel - P.lo0;
+  const float g1 = (py - P.origin1) * P.inv_voxel - P.lo1;
+  const float g2 = (pz - P.origin2) * P.inv_voxel - P.lo2;
+  if (!(g0 >= 0.0f && g0 < C.nf0 && g1 >= 0.0f && g1 < C.nf1 && g2 >= 0.0f && g2 < C.nf2)) return C.out_cost[s];
+  const int k0 = (int)g0, k1 = (int)g1, k2 = (int)g2;  // floor (g >= 0)
+  const float cell = __ldg(sq + ((k0 * P.n1 + k1) * P.n2 + k2));
+  if (cell >= C.far2[s]) return 0.0f;
+  if (cell == 0.0f) return C.zero_cost[s];  // containing cell occupied
   // c = g - 1/2 clamped to [0, n - 1] (vp/mapping.py:654-663)
-  T c0 = g0 - T(0.5), c1 = g1 - T(0.5), c2 = g2 - T(0.5);
-  c0 = fmin(fmax(c0, T(0)), C.chi0);
-  c1 = fmin(fmax(c1, T(0)), C.chi1);
-  c2 = fmin(fmax(c2, T(0)), C.chi2);
-  const T a0 = fmin(floor(c0), C.amax0), a1 = fmin(floor(c1), C.amax1), a2 = fmin(floor(c2), C.amax2);
-  const T f0 = c0 - a0, f1 = c1 - a1, f2 = c2 - a2;  // in [0, 1]
-  const int i0 = (int)a0, i1 = (int)a1, i2 = (int)a2;
-  const float *p = sq + ((i0 * P.n1 + i1) * P.n2 + i2);
-  const float v0 = __ldg(p);
-  if constexpr (sizeof(T) == 4) {
-    // Far-field exit: the field holds exact squared distances between voxel
-    // centres (vpb_edt3d), so sqrt(field) is 1-Lipschitz and every corner of
-    // the cell has sqrt(v) >= sqrt(v0) - sqrt(3); the interpolated distance is
-    // then beyond d_act + r and the term is exactly 0 (the containing cell is
-    // not occupied either).  Most spheres of most steps leave here after one
-    // load instead of eight.
-    if (v0 >= C.far2[s]) return T(0);
-  }
-  const float v1 = __ldg(p + C.off2);
+  const float c0 = fminf(fmaxf(g0 - 0.5f, 0.0f), C.chi0);
+  const float c1 = fminf(fmaxf(g1 - 0.5f, 0.0f), C.chi1);
+  const float c2 = fminf(fmaxf(g2 - 0.5f, 0.0f), C.chi2);
+  const float a0 = fminf(floorf(c0), C.amax0), a1 = fminf(floorf(c1), C.amax1), a2 = fminf(floorf(c2), C.amax2);
+  const float f0 = c0 - a0, f1 = c1 - a1, f2 = c2 - a2;  // in [0, 1]
+  const float *p = sq + (((int)a0 * P.n1 + (int)a1) * P.n2 + (int)a2);
+  const float v0 = __ldg(p), v1 = __ldg(p + C.off2);
   const float *py_ = p + C.off1;
   const float v2 = __ldg(py_), v3 = __ldg(py_ + C.off2);
   const float *px_ = p + C.off0;
   const float v4 = __ldg(px_), v5 = __ldg(px_ + C.off2);
   const float *pxy = px_ + C.off1;
   const float v6 = __ldg(pxy), v7 = __ldg(pxy + C.off2);
-  // containing cell floor(g): the b corner on an axis iff g >= a + 1
-  const bool sx = g0 >= a0 + T(1), sy = g1 >= a1 + T(1), sz = g2 >= a2 + T(1);
-  const float e00 = sz ? v1 : v0, e01 = sz ? v3 : v2, e10 = sz ? v5 : v4, e11 = sz ? v7 : v6;
-  const float e0 = sy ? e01 : e00, e1 = sy ? e11 : e10;
-  const float cell = sx ? e1 : e0;
-  const T h0 = T(1) - f0, h1 = T(1) - f1, h2 = T(1) - f2;
-  const T c00 = fma((T)v4, f0, (T)v0 * h0);
-  const T c01 = fma((T)v5, f0, (T)v1 * h0);
-  const T c10 = fma((T)v6, f0, (T)v2 * h0);
-  const T c11 = fma((T)v7, f0, (T)v3 * h0);
-  const T c0v = fma(c10, f1, c00 * h1);
-  const T c1v = fma(c11, f1, c01 * h1);
-  const T value = fma(c1v, f2, c0v * h2);
-  // branch-free selection (the all-inf field gives inf / NaN -> no cost)
-  T env;
-  if constexpr (sizeof(T) == 8) {
-    const T gap = P.d_act - (P.voxel * sqrt(value) - P.sph_r[s]);
-    env = gap > T(0) ? P.w_env * gap * gap : T(0);
+  const float h0 = 1.0f - f0, h1 = 1.0f - f1, h2 = 1.0f - f2;
+  const float c00 = fmaf(v4, f0, v0 * h0);
+  const float c01 = fmaf(v5, f0, v1 * h0);
+  const float c10 = fmaf(v6, f0, v2 * h0);
+  const float c11 = fmaf(v7, f0, v3 * h0);
+  const float c0v = fmaf(c10, f1, c00 * h1);
+  const float c1v = fmaf(c11, f1, c01 * h1);
+  const float value = fmaf(c1v, f2, c0v * h2);
+  const float dist = P.voxel * (value * rsqrtf(fmaxf(value, 1e-30f)));
+  const float gap = P.d_act - (dist - P.sph_r[s]);
+  return gap > 0.0f ? P.w_env * gap * gap : 0.0f;
+}
+
+template <typename T>
+__device__ __forceinline__ T env_cost(const Prob<T> &P, const FixedConsts<T> &C, const float *sq, int s, T px, T py,
+                                      T pz) {
+  if constexpr (sizeof(T) == 4) {
+    return env_cost_f32(P, C, sq, s, px, py, pz);
   } else {
-    const float dist = P.voxel * (value * rsqrtf(fmaxf(value, 1e-30f)));
-    const float gap = P.d_act - (dist - P.sph_r[s]);
-    env = gap > 0.0f ? P.w_env * gap * gap : 0.0f;
+    const T g0 = (px - P.origin0) / P.voxel - P.lo0;
+    const T g1 = (py - P.origin1) / P.voxel - P.lo1;
+    const T g2 = (pz - P.origin2) / P.voxel - P.lo2;
+    const bool inside = g0 >= T(0) && g0 < C.nf0 && g1 >= T(0) && g1 < C.nf1 && g2 >= T(0) && g2 < C.nf2;
+    const T z0 = inside ? g0 : T(0), z1 = inside ? g1 : T(0), z2 = inside ? g2 : T(0);  // any in-range address
+    // c = g - 1/2 clamped to [0, n - 1] (vp/mapping.py:654-663)
+    T c0 = z0 - T(0.5), c1 = z1 - T(0.5), c2 = z2 - T(0.5);
+    c0 = fmin(fmax(c0, T(0)), C.chi0);
+    c1 = fmin(fmax(c1, T(0)), C.chi1);
+    c2 = fmin(fmax(c2, T(0)), C.chi2);
+    const T a0 = fmin(floor(c0), C.amax0), a1 = fmin(floor(c1), C.amax1), a2 = fmin(floor(c2), C.amax2);
+    const T f0 = c0 - a0, f1 = c1 - a1, f2 = c2 - a2;  // in [0, 1]
+    const float *p = sq + (((int)a0 * P.n1 + (int)a1) * P.n2 + (int)a2);
+    const float v0 = __ldg(p), v1 = __ldg(p + C.off2);
+    const float *py_ = p + C.off1;
+    const float v2 = __ldg(py_), v3 = __ldg(py_ + C.off2);
+    const float *px_ = p + C.off0;
+    const float v4 = __ldg(px_), v5 = __ldg(px_ + C.off2);
+    const float *pxy = px_ + C.off1;
+    const float v6 = __ldg(pxy), v7 = __ldg(pxy + C.off2);
+    // containing cell floor(g): the b corner on an axis iff g >= a + 1
+    const bool sx = z0 >= a0 + T(1), sy = z1 >= a1 + T(1), sz = z2 >= a2 + T(1);
+    const float e00 = sz ? v1 : v0, e01 = sz ? v3 : v2, e10 = sz ? v5 : v4, e11 = sz ? v7 : v6;
+    const float e0 = sy ? e01 : e00, e1 = sy ? e11 : e10;
+    const float cell = sx ? e1 : e0;
+    const T h0 = T(1) - f0, h1 = T(1) - f1, h2 = T(1) - f2;
+    const T c00 = fma((T)v4, f0, (T)v0 * h0);
+    const T c01 = fma((T)v5, f0, (T)v1 * h0);
+    const T c10 = fma((T)v6, f0, (T)v2 * h0);
+    const T c11 = fma((T)v7, f0, (T)v3 * h0);
+    const T c0v = fma(c10, f1, c00 * h1);
+    const T c1v = fma(c11, f1, c01 * h1);
+    const T value = fma(c1v, f2, c0v * h2);
+    // branch-free selection (the all-inf field gives inf / NaN -> no cost)
+    const T gap = P.d_act - (P.voxel * sqrt(value) - P.sph_r[s]);
+    T env = gap > T(0) ? P.w_env * gap * gap : T(0);
+    env = cell == 0.0f ? C.zero_cost[s] : env;
+    return inside ? env : C.out_cost[s];
   }
-  env = cell == 0.0f ? C.zero_cost[s] : env;
-  return inside ? env : C.out_cost[s];
 }
 
 // Which terms of a configuration one warp evaluates (warp-uniform): the
@@ -339,7 +358,7 @@ __device__ __forceinline__ bool fixed_config(const Prob<T> &P, const FixedConsts
       constexpr int i = Topo::pair_i(p), j = Topo::pair_j(p);
       const T dx = cx[i] - cx[j], dy = cy[i] - cy[j], dz = cz[i] - cz[j];
       const T d2 = dx * dx + dy * dy + dz * dz;
-      touch |= d2 < C.rsum2[p] && ((W.pmask >> p) & 1ull);
+      touch |= d2 < C.rsum2[p];  // (the split mask is applied in the exact pass)
     });
     if (touch) {
       static_for<0, NP>([&](auto pc) {
