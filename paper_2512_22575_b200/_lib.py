@@ -9,12 +9,14 @@ current stream handle.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 import numpy as np
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "_lib" / "libvpb200.so"
+# VPB_LIB_PATH: load another build of the library (A/B timing, tools/ab_time.py)
+LIB_PATH = Path(os.environ["VPB_LIB_PATH"]) if os.environ.get("VPB_LIB_PATH") else PKG / "_lib" / "libvpb200.so"
 
 MAX_JOINTS = 16
 MAX_SPHERES = 64
