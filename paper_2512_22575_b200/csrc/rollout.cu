@@ -802,7 +802,7 @@ struct SmpcIO {
   NoiseGen gen;    // on-the-fly perturbations (fixed path) when gen_on
   int gen_on;
   float *eps_out;  // where the drawn perturbations go (== eps for the merge)
-  double *out_host;  // optional host-mapped copy of `out`, written by the last CTA at the end
+  double *out_host;  // optional host-mapped copy of `out` (+ 1 slot: the done flag), written by the last CTA
   double *cand_terms;  // [M][6] per-candidate sums (fixed path): the re-evaluation shortcut
 };
 
@@ -823,6 +823,17 @@ __device__ __forceinline__ void tail_controls(const double *part, const double *
     }
   }
   for (int e = threadIdx.x; e < n; e += blockDim.x) out[hn + n + hn - n + e] = 0.0;
+}
+
+// Zero-copy completion: after every thread's host-mapped writes, one
+// system-scope release (cumulative over the barrier) and the flag word the
+// host spins on (vpb_smpc_session_step).
+__device__ __forceinline__ void signal_host_done(double *flag_slot) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long *>(flag_slot) = 1ull;
+  }
 }
 
 // Diagnostics of the step (thread 0): re-evaluated cost of U* from slot 0 of
@@ -1277,6 +1288,7 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
         __syncthreads();
         const int len = 2 * P.H * P.nj + P.nj + 13;
         for (int e = threadIdx.x; e < len; e += blockDim.x) io.out_host[e] = io.out[e];
+        signal_host_done(io.out_host + len);
       }
     }
   } else {
@@ -1372,6 +1384,7 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
     // (out_host: zero-copy result, posted PCIe writes visible after the kernel completes)
     tail_output(S, rec, P.H, P.nj, best, bad ? (double)io.M : rec[2], io.out, io.out_host);
     fixed_shard_fixup(S, io.M, io.costs, io.flags, nullptr);
+    if (io.out_host) signal_host_done(io.out_host + 2 * P.H * P.nj + P.nj + 13);
     VPB_TRACE(io, 2 * ncta + 2);
   }
 }

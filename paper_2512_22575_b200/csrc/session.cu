@@ -169,7 +169,7 @@ int vpb_smpc_session_create(const vpb_problem *prob, const vpb_field *field, int
   } while (0)
   SESSION_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
   SESSION_CUDA(cudaMallocHost(&s->h_in, (size_t)s->in_len * 8));
-  SESSION_CUDA(cudaMallocHost(&s->h_out, (size_t)s->out_len * 8));
+  SESSION_CUDA(cudaMallocHost(&s->h_out, (size_t)(s->out_len + 1) * 8));  // + the kernel's done flag
   SESSION_CUDA(cudaMalloc(&s->d_in, (size_t)s->in_len * 8));
   SESSION_CUDA(cudaMalloc(&s->d_out, (size_t)s->out_len * 8));
   SESSION_CUDA(cudaMalloc(&s->eps, eps_bytes));
@@ -231,10 +231,25 @@ int vpb_smpc_session_step(vpb_smpc_session *s, const double *q0, const double *q
   // replayed on the caller's stream (NULL = the legacy default stream, as
   // everywhere in this ABI): ordered after whatever produced the field
   cudaStream_t st = vpb::as_stream(stream);
+  volatile uint64_t *done = reinterpret_cast<volatile uint64_t *>(s->h_out + s->out_len);
+  *done = 0;  // the previous launch set it as its last action
   VPB_CUDA(cudaGraphLaunch(s->exec, st));
   double e_pos = 0.0, e_ori = 0.0;  // host diagnostics while the step runs
   vpb_ee_errors(&s->prob, q0, goal_r, goal_t, &e_pos, &e_ori);
-  VPB_CUDA(cudaStreamSynchronize(st));
+  // The kernel's last CTA writes the result into pinned memory and then the
+  // done flag (system-scope release): spin on it instead of waking up from a
+  // stream synchronisation; the stream is polled now and then so an error
+  // (or a kernel variant without the flag) still ends the wait.
+  for (uint32_t spin = 1; *done == 0; ++spin) {
+    if ((spin & 255u) == 0u) {
+      const cudaError_t q = cudaStreamQuery(st);
+      if (q == cudaSuccess) break;
+      if (q != cudaErrorNotReady) {
+        vpb::set_error("smpc session step: %s", cudaGetErrorString(q));
+        return VPB_ERR_CUDA;
+      }
+    }
+  }
   vpb::note_launch(1);
   memcpy(out, s->h_out, (size_t)s->out_len * 8);
   const int64_t base = 2 * s->H * n + n;
