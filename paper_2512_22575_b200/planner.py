@@ -410,24 +410,21 @@ class Planner:
         n = self.chain.dof
         hn = h * n
         base = 2 * hn + n
-        wcost = float(out_host[base])
-        if out_host[base + 9] > 0 or not math.isfinite(wcost):
+        # [cost(U*), 5 sums, terminal, best, Z, non-finite, best index, e_pos, e_ori] as Python floats
+        v = out_host[base:base + 13].tolist()
+        wcost = v[0]
+        if v[9] > 0 or not math.isfinite(wcost):
             raise DegenerateRotation("a sample reached a pose error with rotation angle at pi")
-        terms = out_host[base + 1:base + 7]
-        if not math.isfinite(out_host[base + 11]):  # device-step output: diagnostics on the host
+        if not math.isfinite(v[11]):  # device-step output: diagnostics on the host
             q0 = np.ascontiguousarray(state.q, dtype=np.float64)
             gr = np.ascontiguousarray(goal.rotation.matrix, dtype=np.float64)
             gt = np.ascontiguousarray(goal.translation, dtype=np.float64)
             e = np.zeros(2)
             check(load().vpb_ee_errors(self._base, D.host_ptr(q0), D.host_ptr(gr), D.host_ptr(gt), D.host_ptr(e[:1]),
                                        D.host_ptr(e[1:])), "ee_errors")
-            out_host = out_host.copy()
-            out_host[base + 11:base + 13] = e
-        diag = StepDiagnostics(
-            best_cost=float(out_host[base + 7]), weighted_cost=wcost,
-            breakdown=CostBreakdown(*[float(t) for t in terms]),
-            e_pos=float(out_host[base + 11]), e_ori=float(out_host[base + 12]),
-        )
+            v[11], v[12] = e.tolist()
+        diag = StepDiagnostics(best_cost=v[7], weighted_cost=wcost, breakdown=CostBreakdown(*v[1:7]), e_pos=v[11],
+                               e_ori=v[12])
         return StepResult(command=out_host[hn:hn + n].copy(),
                           next_nominal=out_host[hn + n:2 * hn + n].reshape(h, n).copy(), diagnostics=diag)
 

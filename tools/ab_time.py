@@ -2,6 +2,7 @@
 native-session step, L2 flushed before every timed launch).
 
     python tools/ab_time.py ab/libA.so ab/libB.so [--rounds 4]
+    python tools/ab_time.py lib.so lib.so@VPB_NO_DRY_MERGE=1   (same build, env A/B)
 
 Each round runs every build in its own process (VPB_LIB_PATH), interleaved
 A B A B ... so clock and thermal drift hit all builds alike; prints the
@@ -75,7 +76,11 @@ def main():
     per = {lib: [] for lib in a.libs}
     for _ in range(a.rounds):
         for lib in a.libs:
-            env = dict(os.environ, VPB_LIB_PATH=str(Path(lib).resolve()))
+            path, _, extra = lib.partition("@")
+            env = dict(os.environ, VPB_LIB_PATH=str(Path(path).resolve()))
+            if extra:
+                k, _, v = extra.partition("=")
+                env[k] = v
             r = subprocess.run([sys.executable, __file__, "--worker", "--iters", str(a.iters)], env=env,
                                capture_output=True, text=True, check=True)
             per[lib].append(json.loads(r.stdout.strip().splitlines()[-1]))
