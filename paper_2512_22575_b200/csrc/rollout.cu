@@ -905,10 +905,102 @@ __device__ __forceinline__ void fixed_shard_fixup(const Shared &S, int64_t M, do
   }
 }
 
+// exp() out of line: the large-list expansion unrolls its loads, not this
+__device__ __noinline__ double exp_noinline(double x) { return exp(x); }
+
+// Many nonzero weights (a converged planner: costs within ~746 lam of the
+// minimum) make N = sum_k w_k eps_k an (ncand x H n) reduction -- too much
+// for the merging CTA alone.  The CTAs that took the last kMergeHelpers
+// tickets stay resident, spin on a per-launch flag and, when the merge asks
+// for help, each computes a fixed slice of the N elements over all nonzero
+// candidates (fixed order: deterministic).  Counters after the ticket
+// (io.counters + groups + 2): [epoch, flag = epoch << 2 | state, done, ncand];
+// the epoch advances once per launch, so nothing has to be reset.
+constexpr int kMergeHelpers = 127;
+constexpr int kLightMax = 32;  // up to this many nonzero weights the merging CTA computes N alone
+constexpr int kSliceE = 8;     // N elements per slice pass
+__device__ __forceinline__ int merge_helpers(int ctas) { return ctas - 1 < kMergeHelpers ? ctas - 1 : kMergeHelpers; }
+
+// N elements of participant `part` of `P` (a contiguous slice), over all
+// ncand candidates (lists in global memory), by every thread of the CTA.
+template <typename ET>
+__device__ void n_slice(const SmpcIO &io, const Shared &S, const int *mlist, const double *wlist, int ncand, int hn,
+                        int part, int P, double *dst) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  const ET *eps = reinterpret_cast<const ET *>(io.eps);
+  const int per = (hn + P - 1) / P;
+  const int b0 = part * per, b1 = min(hn, b0 + per);
+  double *red = S.scratch + 152;  // [nw][kSliceE], past the final merge's slots (kFmRed)
+#pragma unroll 1
+  for (int e0 = b0; e0 < b1; e0 += kSliceE) {
+    const int E = min(kSliceE, b1 - e0);
+    double acc[kSliceE];
+#pragma unroll
+    for (int j = 0; j < kSliceE; ++j) acc[j] = 0.0;
+    // 8 candidates per round trip: indices and weights first, then the gathers
+    // (each thread keeps its candidates k = tid + i nt in increasing order)
+#pragma unroll 1
+    for (int k0 = tid; k0 < ncand; k0 += 8 * nt) {
+      int m[8];
+      double w[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int k = k0 + u * nt;
+        m[u] = k < ncand ? __ldcg(mlist + k) : 0;
+        w[u] = k < ncand ? __ldcg(wlist + k) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (w[u] == 0.0) continue;  // zero weights (uncompacted list, padding) add exactly nothing
+        const ET *row = eps + (size_t)m[u] * hn + e0;
+#pragma unroll
+        for (int j = 0; j < kSliceE; ++j)
+          if (j < E) acc[j] += w[u] * load_e<ET>(row + j);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kSliceE; ++j) {
+      const double v = warp_sum_d(acc[j]);
+      if (lane == 0) red[warp * kSliceE + j] = v;
+    }
+    __syncthreads();
+    if (tid < E) {
+      double v = 0.0;
+      for (int w = 0; w < nw; ++w) v += red[w * kSliceE + tid];
+      dst[e0 + tid] = v;
+    }
+    __syncthreads();
+  }
+}
+
+// A helper CTA (one of the last kMergeHelpers finishers): wait for the merge's
+// verdict; on "help", compute slice `part` and report done.
+template <typename ET>
+__device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn, int part, unsigned int ep) {
+  unsigned int *c = io.counters + (ctas + kGroup - 1) / kGroup + 2;
+  unsigned int *st = reinterpret_cast<unsigned int *>(S.misc + 47);
+  if (threadIdx.x == 0) {
+    unsigned int f;
+    while (((f = ld_acquire_gpu(c + 1)) >> 2) != (ep & 0x3fffffffu) || (f & 3u) == 0u) __nanosleep(128);
+    st[0] = f & 3u;
+    st[1] = ld_acquire_gpu(c + 3);
+  }
+  __syncthreads();
+  if (st[0] != 2u) return;
+  const int ncand = (int)st[1];
+  double *gp = io.group_parts;
+  n_slice<ET>(io, S, reinterpret_cast<const int *>(gp + io.M + 64), gp, ncand, hn, part, merge_helpers(ctas) + 1,
+              io.rank_part + kPartHead);
+  if (threadIdx.x == 0) {
+    fence_acq_rel_gpu();
+    atomicAdd(c + 2, 1u);
+  }
+}
+
 // Shared-memory slots of the final merge and the fixed-path tail (S.scratch,
 // kMergeScratch doubles): the merge keeps what the tail needs on chip so the
 // last CTA's chain of dependent global round trips stays short.
-constexpr int kMergeScratch = 64;  // smem_layout scratch argument of smpc_kernel
+constexpr int kMergeScratch = 128;  // smem_layout scratch argument of smpc_kernel (2 * 128 + 24 doubles)
 constexpr int kFmW = 0;            // [32] weights of the first nonzero candidates
 constexpr int kFmCT = 32;          // [6] sums of the minimum's candidate (speculative, for the shortcut)
 constexpr int kFmRec = 40;         // [4] the shard record head: min, Z, non-finite, best index
@@ -916,6 +1008,7 @@ constexpr int kFmBest = 44;        // local index of the minimum's candidate
 constexpr int kFmCL = 48;          // ints: [nw][kFmCap] nonzero CTAs per warp
 constexpr int kFmML = 120;         // ints: [32] indices of the first nonzero candidates
 constexpr int kFmWN = 136;         // ints: [nw] nonzero CTA count per warp
+// (152.. : [nw][kSliceE] N slice reduction, n_slice)
 constexpr int kFmCap = 16;
 
 // Final merge of the single-device step, by the last CTA.  Inputs: the CTA
@@ -933,7 +1026,7 @@ constexpr int kFmCap = 16;
 // warm start are produced in the N pass itself (to out and out_host).
 template <typename ET, int NWC, bool FIXED>
 __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *heads, const double *costs, int ctas,
-                            int hn, int nj, bool fused_u, unsigned long long *trace_head) {
+                            int hn, int nj, bool fused_u, unsigned int ep, unsigned long long *trace_head) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   double *misc = S.misc;
   double *sc = S.scratch;
@@ -1052,68 +1145,12 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   __syncthreads();
   if (trace_head && tid == 0) trace_head[3] = gtimer();
   const int b0c = (b0 >= 0 && b0 < ctas) ? b0 : 0;
-  if (tid < 32) {
-    // 3. (warp 0) the candidates of those CTAs, in order: weights and Z,
-    //    32 candidates per load round trip
-    int off[16];
-    int total = 0;
-    bool small = true;
-    for (int w = 0; w < nw; ++w) {
-      off[w] = total;
-      const int c = wcount[w];
-      small = small && c <= kFmCap;
-      total += c * NWC;
-    }
-    int ncand = 0;
-    double z = 0.0;
-#pragma unroll 1
-    for (int k0 = 0; k0 < total; k0 += 32) {
-      const int k = k0 + lane;
-      int m = -1;
-      double wt = 0.0;
-      if (k < total) {
-        int w = 0;
-        for (int u = 1; u < nw; ++u)
-          if (k >= off[u]) w = u;
-        const int r = k - off[w];
-        const int ci = small ? sclist[w * kFmCap + r / NWC] : clist[w * span + r / NWC];
-        m = ci * NWC + (r % NWC);
-        if (m < io.M) {
-          const double c = costs[m];
-          wt = c < dinf() ? exp(-(c - m0) * inv_lam) : 0.0;
-        }
-      }
-      const unsigned bal = __ballot_sync(kFull, wt != 0.0);
-      if (wt != 0.0) {
-        const int p = ncand + __popc(bal & ((1u << lane) - 1u));
-        mlist[p] = m;
-        wlist[p] = wt;
-        if (p < 32) {
-          smlist[p] = m;
-          sc[kFmW + p] = wt;
-        }
-      }
-      z += wt;  // lane-strided partials in candidate order
-      ncand += __popc(bal);
-    }
-    z = warp_sum_d(z);
-    if (lane == 0) {
-      double *dst = io.rank_part;
-      dst[0] = m0;
-      dst[1] = z;
-      dst[2] = NF;
-      sc[kFmRec + 0] = m0;
-      sc[kFmRec + 1] = z;
-      sc[kFmRec + 2] = NF;
-      misc[42] = (double)ncand;
-      misc[45] = ncand == 1 ? (double)smlist[0] : -1.0;  // the only nonzero weight (U* = nominal + its eps)
-      if (trace_head) trace_head[4] = gtimer();
-    }
-  } else if (warp == 1) {
+  if (warp == 1) {
     // the minimum's global index, and (fixed path) its candidate's sums: when
     // it is the only nonzero weight, they are the re-evaluation of U*
     const double bg = b0 < ctas ? heads[2 * (size_t)ctas + b0c] : -1.0;
-    const int bl = bg >= 0.0 ? (int)(bg - (double)io.m_offset) : -1;
+    const double bd = bg - (double)io.m_offset;
+    const int bl = (bg >= 0.0 && bd < (double)io.M) ? (int)bd : -1;
     if (FIXED && io.cand_terms && lane < 6 && bl >= 0) sc[kFmCT + lane] = __ldcg(io.cand_terms + 6 * (size_t)bl + lane);
     if (lane == 0) {
       sc[kFmRec + 3] = bg;
@@ -1140,41 +1177,167 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
       if (trace_head) trace_head[6] = gtimer();
     }
   }
+  // 3. (all threads) the candidates of those CTAs, in candidate order, NOT
+  //    compacted (a zero weight stays in the list as (m, 0): it adds exactly
+  //    nothing): weights, Z and the nonzero count.  Thread t takes list
+  //    entries t, t + nt, ... (two dependent loads each, batched 8 deep).
+  int total = 0;
+  bool small = true;
+  for (int w = 0; w < nw; ++w) {
+    total += wcount[w] * NWC;
+    small = small && wcount[w] <= kFmCap;
+  }
+  double z = 0.0;
+  int nz = 0;
+  if (total <= 32) {
+    // the usual case (a handful of candidates near the minimum): warp 0,
+    // one entry per lane, one round trip for the CTA index and one for the cost
+    if (warp == 0 && lane < total) {
+      int seg = 0, base = 0;
+      while (seg < nw - 1 && lane >= base + wcount[seg] * NWC) {
+        base += wcount[seg] * NWC;
+        ++seg;
+      }
+      const int r = lane - base;
+      const int ci = small ? sclist[seg * kFmCap + r / NWC] : clist[seg * span + r / NWC];
+      const int m = ci * NWC + (r % NWC);
+      double wt = 0.0;
+      if (m < io.M) {
+        const double c = costs[m];
+        wt = c < dinf() ? exp(-(c - m0) * inv_lam) : 0.0;
+      }
+      const int mm = m < io.M ? m : 0;  // padding slot of the last CTA: weight 0, any valid row
+      mlist[lane] = mm;
+      wlist[lane] = wt;
+      smlist[lane] = mm;
+      sc[kFmW + lane] = wt;
+      z = wt;
+      nz = wt != 0.0 ? 1 : 0;
+    }
+  } else {
+    constexpr int B = 8;
+    int seg = 0, base = 0;  // list segment (warp slice of clist) of entry k; k only grows
+#pragma unroll 1
+    for (int k0 = tid; k0 < total; k0 += B * nt) {
+      int m[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) {  // B independent clist loads
+        const int k = k0 + u * nt;
+        m[u] = -1;
+        if (k < total) {
+          while (seg < nw - 1 && k >= base + wcount[seg] * NWC) {
+            base += wcount[seg] * NWC;
+            ++seg;
+          }
+          const int r = k - base;
+          const int ci = small ? sclist[seg * kFmCap + r / NWC] : clist[seg * span + r / NWC];
+          m[u] = ci * NWC + (r % NWC);
+        }
+      }
+      double c[B];
+#pragma unroll
+      for (int u = 0; u < B; ++u) c[u] = (m[u] >= 0 && m[u] < io.M) ? costs[m[u]] : dinf();  // B independent loads
+#pragma unroll
+      for (int u = 0; u < B; ++u) {
+        const int k = k0 + u * nt;
+        if (k >= total) continue;
+        const double wt = c[u] < dinf() ? exp_noinline(-(c[u] - m0) * inv_lam) : 0.0;
+        const int mm = m[u] < io.M ? m[u] : 0;  // padding slot of the last CTA: weight 0, any valid row
+        mlist[k] = mm;
+        wlist[k] = wt;
+        if (k < kLightMax) {
+          smlist[k] = mm;
+          sc[kFmW + k] = wt;
+        }
+        z += wt;
+        nz += wt != 0.0 ? 1 : 0;
+      }
+    }
+  }
+  z = warp_sum_d(z);
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) nz += __shfl_xor_sync(kFull, nz, d);
+  if (lane == 0) {  // (misc[16..] and [32..] were last read before the compaction barrier)
+    misc[16 + warp] = z;
+    misc[32 + warp] = (double)nz;
+  }
   __syncthreads();
-  if (trace_head && tid == 0) *trace_head = gtimer();
+  if (tid == 0) {
+    double Zs = 0.0, NZ = 0.0;
+    for (int w = 0; w < nw; ++w) {  // fixed warp order
+      Zs += misc[16 + w];
+      NZ += misc[32 + w];
+    }
+    double *dst = io.rank_part;
+    dst[0] = m0;
+    dst[1] = Zs;
+    dst[2] = NF;
+    sc[kFmRec + 0] = m0;
+    sc[kFmRec + 1] = Zs;
+    sc[kFmRec + 2] = NF;
+    misc[42] = (double)total;  // list length (zero weights included)
+    misc[41] = NZ;             // nonzero weights
+    // the only nonzero weight is the minimum's (w = exp(0) = 1): U* = nominal + its eps
+    misc[45] = NZ == 1.0 ? sc[kFmBest] : -1.0;
+    if (trace_head) trace_head[4] = gtimer();
+  }
+  __syncthreads();
   const int ncand = (int)misc[42];
+  const bool heavy = ncand > kLightMax;
+  unsigned int *hc = io.counters + (ctas + kGroup - 1) / kGroup + 2;  // [epoch, flag, done, ncand]
+  const int ph = merge_helpers(ctas);
+  if (tid == 0) {  // verdict to the waiting helper CTAs (the lists are published by the barrier + fence)
+    if (heavy) {  // helpers read the lists and the count after this release
+      hc[3] = (unsigned int)ncand;
+      fence_acq_rel_gpu();
+    }
+    atomicExch(hc + 1, ((ep & 0x3fffffffu) << 2) | (heavy ? 2u : 1u));
+    hc[0] = ep + 1u;  // next launch's epoch (every CTA of this one has read it)
+  }
   if (tid == 32) {
     // record tail: best index and the extension [nonzero count, the single
     // candidate's 6 sums] (lets a multi-device finish skip the re-evaluation)
     double *dst = io.rank_part;
     dst[3] = sc[kFmRec + 3];
     double *ext = dst + kPartHead + hn;
-    const bool one = ncand == 1 && io.cand_terms && (int)sc[kFmBest] == smlist[0];
-    ext[0] = (FIXED && io.cand_terms) ? (double)ncand : -1.0;
+    const double nnz = misc[41];
+    const bool one = nnz == 1.0 && io.cand_terms && sc[kFmBest] >= 0.0;
+    ext[0] = (FIXED && io.cand_terms) ? nnz : -1.0;
     for (int a = 0; a < 6; ++a) ext[1 + a] = one ? sc[kFmCT + a] : 0.0;
   }
   // 4. N = sum_m w_m eps_m over the nonzero candidates, in candidate order
   //    (+ U* = nominal + N / Z, clipped command, shifted warm start)
   const ET *eps = reinterpret_cast<const ET *>(io.eps);
-  const bool sl = ncand <= 32;
-  const int *ml = sl ? smlist : mlist;
-  const double *wl = sl ? sc + kFmW : wlist;
   const double Z = sc[kFmRec + 1];
+  if (heavy) {  // this CTA is the last participant; the helpers do the other slices
+    n_slice<ET>(io, S, mlist, wlist, ncand, hn, ph, ph + 1, io.rank_part + kPartHead);
+    if (tid == 0) {
+      while (ld_acquire_gpu(hc + 2) != (unsigned int)ph) __nanosleep(64);
+      hc[2] = 0u;
+    }
+    __syncthreads();
+  }
 #pragma unroll 1
   for (int e = tid; e < hn; e += nt) {
     double acc = 0.0;
-    int k = 0;
+    if (heavy) {
+      acc = __ldcg(io.rank_part + kPartHead + e);
+    } else {  // <= kLightMax candidates: smem lists
+      const int *ml = smlist;
+      const double *wl = sc + kFmW;
+      int k = 0;
 #pragma unroll 1
-    for (; k + 4 <= ncand; k += 4) {
-      double a[4];
+      for (; k + 4 <= ncand; k += 4) {
+        double a[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) a[t] = load_e<ET>(eps + (size_t)ml[k + t] * hn + e);
+        for (int t = 0; t < 4; ++t) a[t] = load_e<ET>(eps + (size_t)ml[k + t] * hn + e);
 #pragma unroll
-      for (int t = 0; t < 4; ++t) acc += wl[k + t] * a[t];
+        for (int t = 0; t < 4; ++t) acc += wl[k + t] * a[t];
+      }
+#pragma unroll 1
+      for (; k < ncand; ++k) acc += wl[k] * load_e<ET>(eps + (size_t)ml[k] * hn + e);
+      io.rank_part[kPartHead + e] = acc;
     }
-#pragma unroll 1
-    for (; k < ncand; ++k) acc += wl[k] * load_e<ET>(eps + (size_t)ml[k] * hn + e);
-    io.rank_part[kPartHead + e] = acc;
     if (fused_u) {  // tail_controls, element e
       const double u = io.nominal[e] + acc / Z;
       const int64_t o2 = (int64_t)hn + e;  // clipped command (e < nj) / shifted warm start
@@ -1243,20 +1406,32 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
       heads[cta] = mn;
       heads[ctas + cta] = (double)__popc(nfm);
       heads[2 * (size_t)ctas + cta] = mn < dinf() ? (double)(io.m_offset + cta_m0 + bi) : -1.0;
+      // this launch's merge epoch, read before the ticket (it advances only
+      // after the last ticket)
+      const unsigned int ep = *reinterpret_cast<volatile unsigned int *>(io.counters + groups + 2);
       // publication: one gpu-scope release fence + the counter atomic; the
       // CTA taking the last ticket acquires before reading the others' heads
       fence_acq_rel_gpu();
       const unsigned int prev = atomicAdd(&io.counters[groups], 1u);
       const bool last = prev == (unsigned int)(ctas - 1);
       if (last) fence_acq_rel_gpu();
-      flag[0] = last ? 1u : 0u;
+      const int ph = merge_helpers(ctas);
+      const bool helper = !last && (int)prev >= ctas - 1 - ph;
+      flag[0] = last ? 1u : (helper ? 3u : 0u);
+      flag[1] = helper ? (unsigned int)((int)prev - (ctas - 1 - ph)) : 0u;
+      reinterpret_cast<unsigned int *>(S.misc + 46)[0] = ep;
     }
   }
   __syncthreads();
   VPB_TRACE(io, 2 * ctas + 3 + (cta % 4));
   if (flag[0] == 0u) return false;
+  const unsigned int ep = reinterpret_cast<const unsigned int *>(S.misc + 46)[0];
+  if (flag[0] == 3u) {
+    merge_helper<ET>(io, S, ctas, hn, (int)flag[1], ep);
+    return false;
+  }
   VPB_TRACE(io, 2 * ctas);
-  final_merge<ET, NWC, FIXED>(io, S, heads, costs, ctas, hn, nj, FIXED && io.finish,
+  final_merge<ET, NWC, FIXED>(io, S, heads, costs, ctas, hn, nj, FIXED && io.finish, ep,
                               io.trace ? io.trace + 2 * ctas + 13 : nullptr);
   if (threadIdx.x == 0) io.counters[groups] = 0u;
   VPB_TRACE(io, 2 * ctas + 1);
@@ -1782,7 +1957,7 @@ static SmpcWs smpc_ws(void *base, int64_t M, int64_t H, int64_t n) {
   w.pro = reinterpret_cast<double *>(b + o);
   o += align_up((size_t)NWF * 4 * 8, 256);
   w.counters = reinterpret_cast<unsigned int *>(b + o);
-  o += align_up((size_t)(groups + 2) * 4, 256);  // group counters, global counter, prologue flag
+  o += align_up((size_t)(groups + 6) * 4, 256);  // group counters, ticket, prologue flag, merge epoch/flag/done/ncand
   w.bytes = o;
   return w;
 }
@@ -1860,7 +2035,7 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   VPB_REQUIRE(workspace && workspace_bytes >= w.bytes, "workspace too small");
   const int64_t ctas = ceil_div(M, NWF);
   const int64_t groups = ceil_div(ctas, kGroup);
-  if (!counters_zeroed) VPB_CUDA(cudaMemsetAsync(w.counters, 0, (size_t)(groups + 2) * 4, s));
+  if (!counters_zeroed) VPB_CUDA(cudaMemsetAsync(w.counters, 0, (size_t)(groups + 6) * 4, s));
   SmpcIO io;
   memset(&io, 0, sizeof(io));
   io.eps = eps;

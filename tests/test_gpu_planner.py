@@ -229,6 +229,34 @@ def test_smpc_step_vs_golden(pk, precision):
         np.testing.assert_allclose(res.diagnostics.e_ori, diag[3], rtol=1e-9, atol=1e-12)
 
 
+@pytest.mark.parametrize("samples", [4096, 16384])
+def test_all_nonzero_weights_step_equals_explicit_update(pk, samples):
+    """Every weight nonzero (lam = 1e4): the fused step's U* (helper-CTA N
+    reduction) equals soft_weights + update_controls on the same costs, for
+    the one-launch step and for repeated native-session steps (per-launch
+    epochs of the helper protocol)."""
+    pkg, config, mapping, planner, robot = pk
+    from paper_2512_22575_b200.geometry import RigidTransform
+
+    chain, model = config.robot_7dof()
+    params = config.planner_params(7, {"samples": samples, "horizon": 32, "lam": 1e4})
+    pl = planner.Planner(chain, model, params, "fp32")
+    state = robot.JointState.resting(np.full(7, 0.1))
+    goal = RigidTransform.from_vec7([0.3, -0.2, 0.7, 0.9, 0.1, 0.3, -0.2])
+    nom = torch.from_numpy(0.1 * np.sin(np.arange(224)).reshape(32, 7)).cuda()
+    for seed in (3, 4):
+        out, eps = pl.smpc_generate_device(state, goal, None, nom, seed)
+        costs = torch.empty(samples, dtype=torch.float64, device="cuda")
+        pl.smpc_step_device(state, goal, None, nom, eps, costs=costs)
+        w = planner.soft_weights(costs, params.lam)
+        assert int((w > 0).sum()) == samples
+        u = planner.update_controls(nom, eps.double(), w)
+        np.testing.assert_allclose(out[:224].cpu().numpy(), u.cpu().numpy().reshape(-1), rtol=1e-10, atol=1e-12)
+        res = pl.smpc_step(state, goal, None, nom.cpu().numpy(), seed)
+        np.testing.assert_allclose(res.next_nominal.reshape(-1)[:217], out[231:448].cpu().numpy(), rtol=1e-10,
+                                   atol=1e-12)
+
+
 def test_finish_single_weight_shortcut_equals_reevaluation(pk):
     """With one nonzero softmin weight over all ranks (tiny lambda) the
     multi-device finish reuses that candidate's sums from its rank record
@@ -262,14 +290,19 @@ def test_finish_single_weight_shortcut_equals_reevaluation(pk):
     np.testing.assert_allclose(fast, single, rtol=1e-12, atol=1e-14, equal_nan=True)
 
 
-def test_smpc_shard_merge_equals_single(pk):
+@pytest.mark.parametrize("lam", [None, 1e4])
+def test_smpc_shard_merge_equals_single(pk, lam):
     """Sharded partials (2 and 8 shards of one batch) merged in rank order
-    equal the single-device step."""
+    equal the single-device step.  lam = 1e4 makes every
+    weight nonzero: the N reduction then runs on the helper CTAs."""
     pkg, config, mapping, planner, robot = pk
     from paper_2512_22575_b200.geometry import RigidTransform
 
     chain, model = config.robot_7dof()
-    params = config.planner_params(7, {"samples": 1024, "horizon": 20})
+    over = {"samples": 1024, "horizon": 20}
+    if lam is not None:
+        over["lam"] = lam
+    params = config.planner_params(7, over)
     pl = planner.Planner(chain, model, params, "fp32")
     state = robot.JointState.resting(np.full(7, 0.1))
     goal = RigidTransform.from_vec7([0.3, -0.2, 0.7, 0.9, 0.1, 0.3, -0.2])

@@ -18,7 +18,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def worker(iters: int) -> None:
+def worker(iters: int, grid: int, samples: int) -> None:
     sys.path.insert(0, str(ROOT))
     import numpy as np
     import torch
@@ -26,16 +26,16 @@ def worker(iters: int) -> None:
     import bench
     from paper_2512_22575_b200 import _lib
 
-    args = argparse.Namespace(samples=4096, horizon=32, grid=256, precision="fp32")
+    args = argparse.Namespace(samples=samples, horizon=32, grid=grid, precision="fp32")
     dev = torch.device("cuda", 0)
     S = bench.make_scene(args, dev)
     pl, st, goal, field = S["planner"], S["state"], S["goal"], S["field"]
     nom = torch.zeros((32, 7), dtype=torch.float64, device=dev)
     lib = _lib.load()
-    eps = torch.empty((4096, 32, 7), dtype=torch.float32, device=dev)
+    eps = torch.empty((samples, 32, 7), dtype=torch.float32, device=dev)
     out = torch.empty(int(lib.vpb_smpc_out_len(32, 7)), dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-    sess = pl.session(field, 4096)
+    sess = pl.session(field, samples)
     sess.step(st, goal, np.zeros((32, 7)), 0, field)
     stream = torch.cuda.current_stream(dev)
 
@@ -69,9 +69,11 @@ def main():
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--worker", action="store_true")
+    ap.add_argument("--grid", type=int, default=256)
+    ap.add_argument("--samples", type=int, default=4096)
     a = ap.parse_args()
     if a.worker:
-        worker(a.iters)
+        worker(a.iters, a.grid, a.samples)
         return
     per = {lib: [] for lib in a.libs}
     for _ in range(a.rounds):
@@ -81,7 +83,8 @@ def main():
             if extra:
                 k, _, v = extra.partition("=")
                 env[k] = v
-            r = subprocess.run([sys.executable, __file__, "--worker", "--iters", str(a.iters)], env=env,
+            r = subprocess.run([sys.executable, __file__, "--worker", "--iters", str(a.iters), "--grid", str(a.grid),
+                                "--samples", str(a.samples)], env=env,
                                capture_output=True, text=True, check=True)
             per[lib].append(json.loads(r.stdout.strip().splitlines()[-1]))
     summary = {lib: {k: round(statistics.median(x[k] for x in v), 2) for k in v[0]} for lib, v in per.items()}
