@@ -75,6 +75,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Inter-CTA waits of the merge protocol back off with __nanosleep and trap
+// after 2 s: a broken invariant (e.g. counters not zeroed) becomes a CUDA
+// error instead of a hung device.
+struct SpinGuard {
+  unsigned long long t0;
+  __device__ SpinGuard() {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  }
+  __device__ __forceinline__ void pause(unsigned ns) {
+    __nanosleep(ns);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 2000000000ull) __trap();
+  }
+};
 __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int *p) {
   unsigned int v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -981,7 +997,8 @@ __device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn
   unsigned int *st = reinterpret_cast<unsigned int *>(S.misc + 47);
   if (threadIdx.x == 0) {
     unsigned int f;
-    while (((f = ld_acquire_gpu(c + 1)) >> 2) != (ep & 0x3fffffffu) || (f & 3u) == 0u) __nanosleep(128);
+    SpinGuard g;
+    while (((f = ld_acquire_gpu(c + 1)) >> 2) != (ep & 0x3fffffffu) || (f & 3u) == 0u) g.pause(128);
     st[0] = f & 3u;
     st[1] = ld_acquire_gpu(c + 3);
   }
@@ -1161,7 +1178,8 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
     // block 0's q_0 prologue terms (normally long done), summed in split order
     unsigned int *pro_ready = io.counters + (ctas + kGroup - 1) / kGroup + 1;
     if (lane == 0) {
-      while (ld_acquire_gpu(pro_ready) == 0u) __nanosleep(64);
+      SpinGuard g;
+      while (ld_acquire_gpu(pro_ready) == 0u) g.pause(64);
       *pro_ready = 0u;  // counters return to zero for the next launch
     }
     __syncwarp();
@@ -1312,7 +1330,8 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   if (heavy) {  // this CTA is the last participant; the helpers do the other slices
     n_slice<ET>(io, S, mlist, wlist, ncand, hn, ph, ph + 1, io.rank_part + kPartHead);
     if (tid == 0) {
-      while (ld_acquire_gpu(hc + 2) != (unsigned int)ph) __nanosleep(64);
+      SpinGuard g;
+      while (ld_acquire_gpu(hc + 2) != (unsigned int)ph) g.pause(64);
       hc[2] = 0u;
     }
     __syncthreads();
@@ -1402,6 +1421,10 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
         bi = oi;
       }
     }
+    // lanes 1.. wrote costs / flags / sums above: order them before lane 0's
+    // release (__syncwarp orders memory among its threads; the fence is
+    // cumulative only over writes lane 0 has observed)
+    __syncwarp();
     if (w == 0) {
       heads[cta] = mn;
       heads[ctas + cta] = (double)__popc(nfm);

@@ -174,7 +174,12 @@ int vpb_smpc_session_create(const vpb_problem *prob, const vpb_field *field, int
   SESSION_CUDA(cudaMalloc(&s->d_out, (size_t)s->out_len * 8));
   SESSION_CUDA(cudaMalloc(&s->eps, eps_bytes));
   SESSION_CUDA(cudaMalloc(&s->ws, s->ws_bytes));
-  SESSION_CUDA(cudaMemset(s->ws, 0, s->ws_bytes));  // counters: zero once, every launch returns them to zero
+  // The warm-up below runs on the session's non-blocking stream: it must not
+  // overtake the zeroing of its counters nor the field still being built on
+  // the caller's streams (a warm-up on unzeroed counters would spin forever
+  // in the merge protocol).  Creation is rare: synchronise the device.
+  SESSION_CUDA(cudaDeviceSynchronize());
+  SESSION_CUDA(cudaMemsetAsync(s->ws, 0, s->ws_bytes, s->stream));  // counters: zero once, every launch returns them to zero
   memset(s->h_in, 0, (size_t)s->in_len * 8);
   // identity goal so the warm-up launch evaluates a regular pose
   s->h_in[2 * s->n + 0] = s->h_in[2 * s->n + 4] = s->h_in[2 * s->n + 8] = 1.0;
