@@ -929,10 +929,14 @@ __device__ __noinline__ double exp_noinline(double x) { return exp(x); }
 // for the merging CTA alone.  The CTAs that took the last kMergeHelpers
 // tickets stay resident, spin on a per-launch flag and, when the merge asks
 // for help, each computes a fixed slice of the N elements over all nonzero
-// candidates (fixed order: deterministic).  Counters after the ticket
-// (io.counters + groups + 2): [epoch, flag = epoch << 2 | state, done, ncand];
+// candidates (fixed order: deterministic).  Words after the ticket
+// (io.counters + groups + 2): epoch, flag = epoch << 2 | state, ncand, done;
 // the epoch advances once per launch, so nothing has to be reset.
 constexpr int kMergeHelpers = 127;
+// merge words after the ticket and the prologue flag: the epoch shares their
+// line (read once per CTA); the polled flag (+ count) and the done counter
+// get lines of their own so the waiting helpers do not contend with them
+constexpr int kHcFlag = 32, kHcCount = 33, kHcDone = 64, kHcWords = 96;
 constexpr int kLightMax = 32;  // up to this many nonzero weights the merging CTA computes N alone
 constexpr int kSliceE = 8;     // N elements per slice pass
 __device__ __forceinline__ int merge_helpers(int ctas) { return ctas - 1 < kMergeHelpers ? ctas - 1 : kMergeHelpers; }
@@ -998,9 +1002,9 @@ __device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn
   if (threadIdx.x == 0) {
     unsigned int f;
     SpinGuard g;
-    while (((f = ld_acquire_gpu(c + 1)) >> 2) != (ep & 0x3fffffffu) || (f & 3u) == 0u) g.pause(128);
+    while (((f = ld_acquire_gpu(c + kHcFlag)) >> 2) != (ep & 0x3fffffffu) || (f & 3u) == 0u) g.pause(512);
     st[0] = f & 3u;
-    st[1] = ld_acquire_gpu(c + 3);
+    st[1] = ld_acquire_gpu(c + kHcCount);
   }
   __syncthreads();
   if (st[0] != 2u) return;
@@ -1010,7 +1014,7 @@ __device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn
               io.rank_part + kPartHead);
   if (threadIdx.x == 0) {
     fence_acq_rel_gpu();
-    atomicAdd(c + 2, 1u);
+    atomicAdd(c + kHcDone, 1u);
   }
 }
 
@@ -1302,14 +1306,14 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   __syncthreads();
   const int ncand = (int)misc[42];
   const bool heavy = ncand > kLightMax;
-  unsigned int *hc = io.counters + (ctas + kGroup - 1) / kGroup + 2;  // [epoch, flag, done, ncand]
+  unsigned int *hc = io.counters + (ctas + kGroup - 1) / kGroup + 2;  // merge words (kHc*)
   const int ph = merge_helpers(ctas);
   if (tid == 0) {  // verdict to the waiting helper CTAs (the lists are published by the barrier + fence)
     if (heavy) {  // helpers read the lists and the count after this release
-      hc[3] = (unsigned int)ncand;
+      hc[kHcCount] = (unsigned int)ncand;
       fence_acq_rel_gpu();
     }
-    atomicExch(hc + 1, ((ep & 0x3fffffffu) << 2) | (heavy ? 2u : 1u));
+    *reinterpret_cast<volatile unsigned int *>(hc + kHcFlag) = ((ep & 0x3fffffffu) << 2) | (heavy ? 2u : 1u);
     hc[0] = ep + 1u;  // next launch's epoch (every CTA of this one has read it)
   }
   if (tid == 32) {
@@ -1331,8 +1335,8 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
     n_slice<ET>(io, S, mlist, wlist, ncand, hn, ph, ph + 1, io.rank_part + kPartHead);
     if (tid == 0) {
       SpinGuard g;
-      while (ld_acquire_gpu(hc + 2) != (unsigned int)ph) g.pause(64);
-      hc[2] = 0u;
+      while (ld_acquire_gpu(hc + kHcDone) != (unsigned int)ph) g.pause(64);
+      hc[kHcDone] = 0u;
     }
     __syncthreads();
   }
@@ -1393,6 +1397,9 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
   double *costs = io.costs ? io.costs : io.cand_costs;
   unsigned int *flag = reinterpret_cast<unsigned int *>(S.misc + 44);
   if (threadIdx.x < 32) {
+    // this launch's merge epoch (it advances only after the last ticket):
+    // loaded first so its latency hides under the candidate writes below
+    const unsigned int ep = threadIdx.x == 0 ? *reinterpret_cast<volatile unsigned int *>(io.counters + groups + 2) : 0u;
     const int w = threadIdx.x;
     const int64_t m = cta_m0 + w;
     double c = dinf();
@@ -1429,9 +1436,6 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
       heads[cta] = mn;
       heads[ctas + cta] = (double)__popc(nfm);
       heads[2 * (size_t)ctas + cta] = mn < dinf() ? (double)(io.m_offset + cta_m0 + bi) : -1.0;
-      // this launch's merge epoch, read before the ticket (it advances only
-      // after the last ticket)
-      const unsigned int ep = *reinterpret_cast<volatile unsigned int *>(io.counters + groups + 2);
       // publication: one gpu-scope release fence + the counter atomic; the
       // CTA taking the last ticket acquires before reading the others' heads
       fence_acq_rel_gpu();
@@ -1980,7 +1984,7 @@ static SmpcWs smpc_ws(void *base, int64_t M, int64_t H, int64_t n) {
   w.pro = reinterpret_cast<double *>(b + o);
   o += align_up((size_t)NWF * 4 * 8, 256);
   w.counters = reinterpret_cast<unsigned int *>(b + o);
-  o += align_up((size_t)(groups + 6) * 4, 256);  // group counters, ticket, prologue flag, merge epoch/flag/done/ncand
+  o += align_up((size_t)(groups + 2 + kHcWords) * 4, 256);  // group counters, ticket, prologue flag, merge words
   w.bytes = o;
   return w;
 }
@@ -2058,7 +2062,7 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   VPB_REQUIRE(workspace && workspace_bytes >= w.bytes, "workspace too small");
   const int64_t ctas = ceil_div(M, NWF);
   const int64_t groups = ceil_div(ctas, kGroup);
-  if (!counters_zeroed) VPB_CUDA(cudaMemsetAsync(w.counters, 0, (size_t)(groups + 6) * 4, s));
+  if (!counters_zeroed) VPB_CUDA(cudaMemsetAsync(w.counters, 0, (size_t)(groups + 2 + kHcWords) * 4, s));
   SmpcIO io;
   memset(&io, 0, sizeof(io));
   io.eps = eps;
