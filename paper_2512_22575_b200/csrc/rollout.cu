@@ -950,7 +950,9 @@ __device__ void n_slice(const SmpcIO &io, const Shared &S, const int *mlist, con
   const ET *eps = reinterpret_cast<const ET *>(io.eps);
   const int per = (hn + P - 1) / P;
   const int b0 = part * per, b1 = min(hn, b0 + per);
-  double *red = S.scratch + 152;  // [nw][kSliceE], past the final merge's slots (kFmRed)
+  // [nw][kSliceE] over the merge's CTA-list slots (kFmCL.., free once the
+  // list is expanded); the record head at kFmRec stays intact
+  double *red = S.scratch + 48;
 #pragma unroll 1
   for (int e0 = b0; e0 < b1; e0 += kSliceE) {
     const int E = min(kSliceE, b1 - e0);
@@ -1021,7 +1023,7 @@ __device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn
 // Shared-memory slots of the final merge and the fixed-path tail (S.scratch,
 // kMergeScratch doubles): the merge keeps what the tail needs on chip so the
 // last CTA's chain of dependent global round trips stays short.
-constexpr int kMergeScratch = 128;  // smem_layout scratch argument of smpc_kernel (2 * 128 + 24 doubles)
+constexpr int kMergeScratch = 64;  // smem_layout scratch argument of smpc_kernel (2 * 64 + 24 doubles)
 constexpr int kFmW = 0;            // [32] weights of the first nonzero candidates
 constexpr int kFmCT = 32;          // [6] sums of the minimum's candidate (speculative, for the shortcut)
 constexpr int kFmRec = 40;         // [4] the shard record head: min, Z, non-finite, best index
@@ -1029,7 +1031,8 @@ constexpr int kFmBest = 44;        // local index of the minimum's candidate
 constexpr int kFmCL = 48;          // ints: [nw][kFmCap] nonzero CTAs per warp
 constexpr int kFmML = 120;         // ints: [32] indices of the first nonzero candidates
 constexpr int kFmWN = 136;         // ints: [nw] nonzero CTA count per warp
-// (152.. : [nw][kSliceE] N slice reduction, n_slice)
+// (48..120 again, after the expansion: [nw][kSliceE] N slice reduction, n_slice)
+// smem per CTA must stay under 48 KB / 7 so that 7 CTAs fit the default carveout
 constexpr int kFmCap = 16;
 
 // Final merge of the single-device step, by the last CTA.  Inputs: the CTA
