@@ -1282,17 +1282,9 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   z = warp_sum_d(z);
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) nz += __shfl_xor_sync(kFull, nz, d);
-  if (lane == 0) {  // (misc[16..] and [32..] were last read before the compaction barrier)
-    misc[16 + warp] = z;
-    misc[32 + warp] = (double)nz;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double Zs = 0.0, NZ = 0.0;
-    for (int w = 0; w < nw; ++w) {  // fixed warp order
-      Zs += misc[16 + w];
-      NZ += misc[32 + w];
-    }
+  // the record head: written by warp 0 alone for a short list (one barrier),
+  // after a fixed-order sum over the warps otherwise
+  auto write_head = [&](double Zs, double NZ) {
     double *dst = io.rank_part;
     dst[0] = m0;
     dst[1] = Zs;
@@ -1300,14 +1292,28 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
     sc[kFmRec + 0] = m0;
     sc[kFmRec + 1] = Zs;
     sc[kFmRec + 2] = NF;
-    misc[42] = (double)total;  // list length (zero weights included)
-    misc[41] = NZ;             // nonzero weights
-    // the only nonzero weight is the minimum's (w = exp(0) = 1): U* = nominal + its eps
-    misc[45] = NZ == 1.0 ? sc[kFmBest] : -1.0;
+    misc[41] = NZ;  // nonzero weights (the only one, if NZ == 1, is the minimum's: sc[kFmBest])
     if (trace_head) trace_head[4] = gtimer();
+  };
+  if (total <= 32) {
+    if (tid == 0) write_head(z, (double)nz);
+  } else {
+    if (lane == 0) {  // (misc[16..] and [32..] were last read before the compaction barrier)
+      misc[16 + warp] = z;
+      misc[32 + warp] = (double)nz;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double Zs = 0.0, NZ = 0.0;
+      for (int w = 0; w < nw; ++w) {  // fixed warp order
+        Zs += misc[16 + w];
+        NZ += misc[32 + w];
+      }
+      write_head(Zs, NZ);
+    }
   }
   __syncthreads();
-  const int ncand = (int)misc[42];
+  const int ncand = total;  // list length (zero weights included)
   const bool heavy = ncand > kLightMax;
   unsigned int *hc = io.counters + (ctas + kGroup - 1) / kGroup + 2;  // merge words (kHc*)
   const int ph = merge_helpers(ctas);
@@ -1549,7 +1555,8 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
       // Z = 1, so U* = nominal + eps_best exactly and its re-evaluation is the
       // best candidate's own evaluation -- reuse its sums (fetched by the
       // merge when that candidate is the minimum's, as it must be).
-      const int single = (int)S.misc[45];
+      // the only nonzero weight is the minimum's (w = exp(0) = 1): U* = nominal + its eps
+      const int single = S.misc[41] == 1.0 ? (int)S.scratch[kFmBest] : -1;
       if (single >= 0 && S.scratch[kFmRec + 1] == 1.0) {
         if (threadIdx.x < NWF) {
           const bool spec = (int)S.scratch[kFmBest] == single;
