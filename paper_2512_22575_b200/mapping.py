@@ -352,6 +352,7 @@ class DistanceField:
         o.flags.writeable = False
         object.__setattr__(self, "origin", o)
         object.__setattr__(self, "_sq_host", None)
+        object.__setattr__(self, "_sq_ptr", self.sq_device.data_ptr())  # the per-step native call passes it
 
     @property
     def sq(self) -> np.ndarray:

@@ -635,13 +635,15 @@ class SmpcSession:
                                         planner._prec, ctypes.byref(handle)), "smpc_session_create")
         self._h = handle
         self.out = np.zeros(int(L.vpb_smpc_session_out_len(self.h, self.n)))
-        self._q0 = np.zeros(self.n)
-        self._qd0 = np.zeros(self.n)
-        self._gr = np.zeros(9)
-        self._gt = np.zeros(3)
+        # [q0 (n) | qd0 (n) | goal R (9) | goal t (3)]: filled by one concatenate per step
+        self._blk = np.zeros(2 * self.n + 12)
+        self._q0, self._qd0 = self._blk[:self.n], self._blk[self.n:2 * self.n]
+        self._gr, self._gt = self._blk[2 * self.n:2 * self.n + 9], self._blk[2 * self.n + 9:]
+        self._nom = np.zeros((self.h, self.n))
         # the per-step call passes plain integers (no per-call ctypes objects)
         self._p_q0, self._p_qd0 = self._q0.ctypes.data, self._qd0.ctypes.data
         self._p_gr, self._p_gt, self._p_out = self._gr.ctypes.data, self._gt.ctypes.data, self.out.ctypes.data
+        self._p_nom = self._nom.ctypes.data
         self._step = L.vpb_smpc_session_step
         self._dev_index = planner.device.index if planner.device.index is not None else torch.cuda.current_device()
 
@@ -650,15 +652,11 @@ class SmpcSession:
         q0, qd0 = state.q, state.qd
         if q0.shape != (n,) or qd0.shape != (n,):
             raise DimensionMismatch("state does not match the chain's dof")
-        self._q0[:] = q0
-        self._qd0[:] = qd0
-        self._gr[:] = goal.rotation.matrix.reshape(-1)
-        self._gt[:] = goal.translation
-        nom = nominal if (nominal.dtype == np.float64 and nominal.flags.c_contiguous) else \
-            np.ascontiguousarray(nominal, dtype=np.float64)
+        np.concatenate((q0, qd0, goal.rotation.matrix.reshape(-1), goal.translation), out=self._blk)
+        self._nom[...] = nominal
         f = _field_of(snap)
-        sq = f.sq_device.data_ptr() if f is not None else None
-        rc = self._step(self._h, self._p_q0, self._p_qd0, self._p_gr, self._p_gt, nom.ctypes.data,
+        sq = f._sq_ptr if f is not None else None
+        rc = self._step(self._h, self._p_q0, self._p_qd0, self._p_gr, self._p_gt, self._p_nom,
                         int(rng_seed) & 0xFFFFFFFFFFFFFFFF, sq, self._p_out, _raw_stream(self._dev_index))
         if rc:
             check(rc, "smpc_session_step")
