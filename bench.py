@@ -300,7 +300,7 @@ def run_ours(args):
     graph = None
     if world == 1:
         # the production path: the native session's captured step graph
-        # (H2D of the 0.4 KB per-call block -> fused step kernel that draws the
+        # (H2D of the 1.8 KB per-call block -> fused step kernel that draws the
         # noise and writes the result into pinned host memory), replayed on
         # the stream with the inputs staged by one public-API step
         graph = pl.session(field, M)
