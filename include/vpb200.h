@@ -259,6 +259,14 @@ int vpb_smpc_generate(const vpb_problem *prob, const vpb_field *field, uint64_t 
                       int precision, double *costs, uint8_t *flags, void *eps_out, double *part_out, double *out,
                       void *workspace, size_t workspace_bytes, void *stream);
 
+/* Debug export of the softmin weights of the last single-device step run on
+ * `workspace` (vpb_smpc_step / vpb_smpc_generate with `out`): weights (dev,
+ * M f64) receives w_m = exp(-(S_m - min S)/lam) / Z exactly as the fused
+ * merge computed them (zeros for the candidates it proved negligible).  Test
+ * infrastructure for the weight parity of vp/planner.py:373-384. */
+int vpb_smpc_debug_weights(const vpb_problem *prob, int64_t M, const void *workspace, size_t workspace_bytes,
+                           double *weights, void *stream);
+
 /* Multi-device finish: merge R rank partials (R x partial_len, dev) in rank
  * order and run the same tail as vpb_smpc_step into `out`. */
 size_t vpb_smpc_finish_workspace_bytes(int64_t n_parts, int64_t H, int64_t n);

@@ -117,6 +117,7 @@ SIGNATURES = {
     "vpb_sample_perturbations": (ctypes.c_int, [ctypes.c_uint64, _p, _i64, _i64, _i64, _i64, _i64, _p,
                                                 ctypes.c_int, _p, _p]),
     "vpb_debug_smpc_trace": (None, [_p]),
+    "vpb_smpc_debug_weights": (ctypes.c_int, [_P(VpbProblem), _i64, _p, _sz, _p, _p]),
     "vpb_pixel_scratch_bytes": (_i64, [_i64, _i64]),
     "vpb_smpc_session_out_len": (_i64, [_i64, _i64]),
     "vpb_smpc_session_create": (ctypes.c_int, [_P(VpbProblem), _P(VpbField), _i64, _i64, _p, ctypes.c_int,

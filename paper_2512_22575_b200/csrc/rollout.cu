@@ -820,6 +820,7 @@ struct SmpcIO {
   float *eps_out;  // where the drawn perturbations go (== eps for the merge)
   double *out_host;  // optional host-mapped copy of `out` (+ 1 slot: the done flag), written by the last CTA
   double *cand_terms;  // [M][6] per-candidate sums (fixed path): the re-evaluation shortcut
+  int max_helpers;     // helper CTAs of the heavy merge (residency-capped, see merge_helpers)
 };
 
 // U* = nominal + N / Z, the clipped command and the shifted warm start
@@ -939,7 +940,12 @@ constexpr int kMergeHelpers = 127;
 constexpr int kHcFlag = 32, kHcCount = 33, kHcDone = 64, kHcWords = 96;
 constexpr int kLightMax = 32;  // up to this many nonzero weights the merging CTA computes N alone
 constexpr int kSliceE = 8;     // N elements per slice pass
-__device__ __forceinline__ int merge_helpers(int ctas) { return ctas - 1 < kMergeHelpers ? ctas - 1 : kMergeHelpers; }
+// io.max_helpers (host: min(kMergeHelpers, resident CTA slots - 2)) keeps the
+// spinning helpers from filling every slot while CTAs without a ticket still
+// wait to be scheduled (small MIG / MPS partitions); 0 = the merger alone
+__device__ __forceinline__ int merge_helpers(const SmpcIO &io, int ctas) {
+  return ctas - 1 < io.max_helpers ? ctas - 1 : io.max_helpers;
+}
 
 // N elements of participant `part` of `P` (a contiguous slice), over all
 // ncand candidates (lists in global memory), by every thread of the CTA.
@@ -1012,7 +1018,7 @@ __device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn
   if (st[0] != 2u) return;
   const int ncand = (int)st[1];
   double *gp = io.group_parts;
-  n_slice<ET>(io, S, reinterpret_cast<const int *>(gp + io.M + 64), gp, ncand, hn, part, merge_helpers(ctas) + 1,
+  n_slice<ET>(io, S, reinterpret_cast<const int *>(gp + io.M + 64), gp, ncand, hn, part, merge_helpers(io, ctas) + 1,
               io.rank_part + kPartHead);
   if (threadIdx.x == 0) {
     fence_acq_rel_gpu();
@@ -1316,12 +1322,11 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   const int ncand = total;  // list length (zero weights included)
   const bool heavy = ncand > kLightMax;
   unsigned int *hc = io.counters + (ctas + kGroup - 1) / kGroup + 2;  // merge words (kHc*)
-  const int ph = merge_helpers(ctas);
+  const int ph = merge_helpers(io, ctas);
   if (tid == 0) {  // verdict to the waiting helper CTAs (the lists are published by the barrier + fence)
-    if (heavy) {  // helpers read the lists and the count after this release
-      hc[kHcCount] = (unsigned int)ncand;
-      fence_acq_rel_gpu();
-    }
+    // list length: read by the helpers (heavy) and by vpb_smpc_debug_weights
+    hc[kHcCount] = (unsigned int)ncand;
+    if (heavy) fence_acq_rel_gpu();  // helpers read the lists and the count after this release
     *reinterpret_cast<volatile unsigned int *>(hc + kHcFlag) = ((ep & 0x3fffffffu) << 2) | (heavy ? 2u : 1u);
     hc[0] = ep + 1u;  // next launch's epoch (every CTA of this one has read it)
   }
@@ -1451,7 +1456,7 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
       const unsigned int prev = atomicAdd(&io.counters[groups], 1u);
       const bool last = prev == (unsigned int)(ctas - 1);
       if (last) fence_acq_rel_gpu();
-      const int ph = merge_helpers(ctas);
+      const int ph = merge_helpers(io, ctas);
       const bool helper = !last && (int)prev >= ctas - 1 - ph;
       flag[0] = last ? 1u : (helper ? 3u : 0u);
       flag[1] = helper ? (unsigned int)((int)prev - (ctas - 1 - ph)) : 0u;
@@ -1918,24 +1923,52 @@ static int launch_rollout_t(const Prob<T> &P, const RolloutIO &io, int topo, cud
   return check_launch("rollout_kernel");
 }
 
+// Resident CTA slots of kernel k on the current device (occupancy x SMs),
+// cached per (kernel, device, smem): the helper cap of the merge protocol.
+template <typename K>
+static int resident_slots(K k, int threads, size_t smem) {
+  static thread_local const void *c_k = nullptr;
+  static thread_local int c_dev = -1, c_slots = 0;
+  static thread_local size_t c_smem = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (c_k == (const void *)k && c_dev == dev && c_smem == smem) return c_slots;
+  int per_sm = 0, sms = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  c_k = (const void *)k;
+  c_dev = dev;
+  c_smem = smem;
+  c_slots = per_sm * sms;
+  return c_slots;
+}
+
 template <typename T, typename ET>
 static int launch_smpc_t(const Prob<T> &P, const SmpcIO &io, int topo, cudaStream_t s) {
   const int64_t ctas = ceil_div(io.M, topo ? NWF : NW) + (topo ? 1 : 0);  // fixed path: + prologue block
-  const int groups = (int)ceil_div(ctas, kGroup);
   const size_t smem = smem_bytes(P, kMergeScratch, topo);
   int rc;
+  auto go = [&](auto k, int threads) {
+    SmpcIO io2 = io;
+    const int slots = resident_slots(k, threads, smem);
+    io2.max_helpers = slots - 2 < kMergeHelpers ? (slots - 2 > 0 ? slots - 2 : 0) : kMergeHelpers;
+    k<<<(unsigned)ctas, threads, smem, s>>>(P, io2);
+  };
   if (topo == 1) {
     auto k = smpc_kernel<T, ET, 8, TopoRobot7>;
     if ((rc = set_smem(k, smem))) return rc;
-    k<<<(unsigned)ctas, smpc_threads<TopoRobot7>(), smem, s>>>(P, io);
+    go(k, smpc_threads<TopoRobot7>());
   } else if (P.nj <= 8) {
     auto k = smpc_kernel<T, ET, 8, TopoDyn>;
     if ((rc = set_smem(k, smem))) return rc;
-    k<<<(unsigned)ctas, kThreads, smem, s>>>(P, io);
+    go(k, kThreads);
   } else {
     auto k = smpc_kernel<T, ET, kMaxJ, TopoDyn>;
     if ((rc = set_smem(k, smem))) return rc;
-    k<<<(unsigned)ctas, kThreads, smem, s>>>(P, io);
+    go(k, kThreads);
   }
   return check_launch("smpc_kernel");
 }
@@ -2158,6 +2191,40 @@ int vpb_smpc_generate(const vpb_problem *prob, const vpb_field *field, uint64_t 
                      workspace, workspace_bytes, s);
 }
 
+}  // extern "C"
+
+namespace vpb {
+// Debug export of the fused step's softmin weights: the final merge leaves
+// its weight list (w_k = exp(-(S_k - min)/lam), uncompacted, zero weights
+// included) and candidate indices in the workspace and the list length in
+// the merge words; w_m / Z is scattered to weights[m].
+__global__ void debug_weights_kernel(const double *wlist, const int *mlist, const unsigned int *ncand_p,
+                                     const double *rank_part, double *weights) {
+  const int ncand = (int)*ncand_p;
+  const double Z = rank_part[1];
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < ncand; k += gridDim.x * blockDim.x) {
+    const double w = wlist[k];
+    if (w != 0.0) weights[mlist[k]] = w / Z;  // zero-weight padding slots may alias sample 0
+  }
+}
+}  // namespace vpb
+
+extern "C" {
+int vpb_smpc_debug_weights(const vpb_problem *prob, int64_t M, const void *workspace, size_t workspace_bytes,
+                           double *weights, void *stream) {
+  VPB_REQUIRE(prob && workspace && weights && M >= 1, "bad arguments to vpb_smpc_debug_weights");
+  const SmpcWs w = smpc_ws(const_cast<void *>(workspace), M, prob->horizon, prob->n_joints);
+  VPB_REQUIRE(workspace_bytes >= w.bytes, "workspace too small");
+  const int topo = fixed_topology_disabled() ? 0 : topo_id(prob);
+  const int64_t ctas = ceil_div(M, topo ? NWF : NW);
+  const int64_t groups = ceil_div(ctas, kGroup);
+  const unsigned int *hc = w.counters + groups + 2;
+  cudaStream_t s = as_stream(stream);
+  VPB_CUDA(cudaMemsetAsync(weights, 0, (size_t)M * 8, s));
+  debug_weights_kernel<<<(unsigned)(ceil_div(M, 256) < 1024 ? ceil_div(M, 256) : 1024), 256, 0, s>>>(
+      w.group_parts, reinterpret_cast<const int *>(w.group_parts + M + 64), hc + kHcCount, w.rank_part, weights);
+  return check_launch("debug_weights_kernel");
+}
 }  // extern "C"
 
 namespace vpb {

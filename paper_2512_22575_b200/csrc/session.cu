@@ -22,6 +22,8 @@ struct vpb_smpc_session {
   double sigma[VPB_MAX_JOINTS];
   cudaStream_t stream;
   cudaGraphExec_t exec;
+  cudaEvent_t launched;  // recorded after an asynchronous vpb_smpc_session_launch
+  bool inflight;         // a launch() replay may still read h_in / write h_out
   double *h_in, *d_in;  // [dyn (2n + 12) | seed bits | field pointer bits | nominal (H n)]
   double *h_out, *d_out;
   void *eps, *ws;
@@ -33,6 +35,8 @@ namespace {
 
 void release(vpb_smpc_session *s) {
   if (!s) return;
+  if (s->inflight) cudaEventSynchronize(s->launched);
+  if (s->launched) cudaEventDestroy(s->launched);
   if (s->exec) cudaGraphExecDestroy(s->exec);
   if (s->stream) cudaStreamDestroy(s->stream);
   cudaFreeHost(s->h_in);
@@ -168,6 +172,7 @@ int vpb_smpc_session_create(const vpb_problem *prob, const vpb_field *field, int
     }                                                                       \
   } while (0)
   SESSION_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  SESSION_CUDA(cudaEventCreateWithFlags(&s->launched, cudaEventDisableTiming));
   SESSION_CUDA(cudaMallocHost(&s->h_in, (size_t)s->in_len * 8));
   SESSION_CUDA(cudaMallocHost(&s->h_out, (size_t)(s->out_len + 1) * 8));  // + the kernel's done flag
   SESSION_CUDA(cudaMalloc(&s->d_in, (size_t)s->in_len * 8));
@@ -220,6 +225,10 @@ int vpb_smpc_session_step(vpb_smpc_session *s, const double *q0, const double *q
                           const double *goal_t, const double *nominal, uint64_t seed, const float *field_sq,
                           double *out, void *stream) {
   VPB_REQUIRE(s && q0 && qd0 && goal_r && goal_t && out, "null argument to vpb_smpc_session_step");
+  if (s->inflight) {  // an asynchronous launch() may still read h_in and set the done flag
+    VPB_CUDA(cudaEventSynchronize(s->launched));
+    s->inflight = false;
+  }
   const int64_t n = s->n;
   double *h = s->h_in;
   memcpy(h, q0, n * 8);
@@ -245,7 +254,9 @@ int vpb_smpc_session_step(vpb_smpc_session *s, const double *q0, const double *q
   // done flag (system-scope release): spin on it instead of waking up from a
   // stream synchronisation; the stream is polled now and then so an error
   // (or a kernel variant without the flag) still ends the wait.
-  for (uint32_t spin = 1; *done == 0; ++spin) {
+  // acquire: the payload loads below must not be satisfied before the flag
+  // load (weakly ordered hosts, e.g. Grace)
+  for (uint32_t spin = 1; __atomic_load_n(const_cast<const uint64_t *>(done), __ATOMIC_ACQUIRE) == 0; ++spin) {
     if ((spin & 255u) == 0u) {
       const cudaError_t q = cudaStreamQuery(st);
       if (q == cudaSuccess) break;
@@ -255,6 +266,7 @@ int vpb_smpc_session_step(vpb_smpc_session *s, const double *q0, const double *q
       }
     }
   }
+  std::atomic_thread_fence(std::memory_order_acquire);  // also covers the stream-query exit
   vpb::note_launch(1);
   memcpy(out, s->h_out, (size_t)s->out_len * 8);
   const int64_t base = 2 * s->H * n + n;
@@ -265,7 +277,12 @@ int vpb_smpc_session_step(vpb_smpc_session *s, const double *q0, const double *q
 
 int vpb_smpc_session_launch(vpb_smpc_session *s, void *stream) {
   VPB_REQUIRE(s, "null session");
-  VPB_CUDA(cudaGraphLaunch(s->exec, vpb::as_stream(stream)));
+  // (replays of this graph are ordered on the stream and none rewrites h_in,
+  // so back-to-back launches need no wait; step() waits for the last one)
+  cudaStream_t st = vpb::as_stream(stream);
+  VPB_CUDA(cudaGraphLaunch(s->exec, st));
+  VPB_CUDA(cudaEventRecord(s->launched, st));
+  s->inflight = true;
   vpb::note_launch(1);
   return VPB_OK;
 }

@@ -227,6 +227,7 @@ class Planner:
         self._base = pack_problem(chain, model, params)
         self._sessions: dict = {}
         self._last_session = None
+        self._ws: dict = {}
 
     def problem(self, state: JointState | None, goal: RigidTransform | None, horizon: int | None = None,
                 dyn: torch.Tensor | None = None) -> VpbProblem:
@@ -322,8 +323,34 @@ class Planner:
         return out
 
     def _smpc_ws(self, m: int, h: int) -> torch.Tensor:
-        L = load()
-        return D.Workspace.get(self.device, f"smpc-{m}-{h}", int(L.vpb_smpc_workspace_bytes(m, h, self.chain.dof)))
+        """This planner's step workspace for (M, H): owned by the planner (not
+        shared between planners or graphs), fixed size per key, so a captured
+        graph's pointers into it stay valid for the planner's lifetime."""
+        ws = self._ws.get((m, h))
+        if ws is None:
+            nbytes = int(load().vpb_smpc_workspace_bytes(m, h, self.chain.dof))
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws[(m, h)] = ws
+        return ws
+
+    def _finish_ws(self, n_parts: int, h: int) -> torch.Tensor:
+        ws = self._ws.get(("finish", n_parts, h))
+        if ws is None:
+            nbytes = int(load().vpb_smpc_finish_workspace_bytes(n_parts, h, self.chain.dof))
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+            self._ws[("finish", n_parts, h)] = ws
+        return ws
+
+    def smpc_weights_device(self, m: int, h: int) -> torch.Tensor:
+        """Softmin weights (M,) f64 of the last single-device step run with M
+        samples and horizon H, as the fused merge computed them (debug export,
+        vpb_smpc_debug_weights)."""
+        ws = self._smpc_ws(m, h)
+        w = torch.empty(m, dtype=torch.float64, device=self.device)
+        P = self.problem(None, None, horizon=h)
+        check(load().vpb_smpc_debug_weights(P, m, D.ptr(ws), ws.numel(), D.ptr(w), D.stream(self.device)),
+              "smpc_debug_weights")
+        return w
 
     def smpc_partial_device(self, state, goal, snap, nominal_dev: torch.Tensor, eps_dev: torch.Tensor,
                             m_offset: int = 0, dyn: torch.Tensor | None = None):
@@ -397,8 +424,7 @@ class Planner:
         if out is None:
             out = torch.empty(int(L.vpb_smpc_out_len(h, n)), dtype=torch.float64, device=self.device)
         parts = partials.reshape(-1, int(L.vpb_smpc_partial_len(h, n))).contiguous()
-        ws_bytes = int(L.vpb_smpc_finish_workspace_bytes(parts.shape[0], h, n))
-        ws = D.Workspace.get(self.device, "smpc_finish", ws_bytes)
+        ws = self._finish_ws(parts.shape[0], h)
         check(L.vpb_smpc_finish(P, _field_struct(snap), D.ptr(parts), parts.shape[0], D.ptr(nominal_dev),
                                 self._prec, D.ptr(out), D.ptr(ws), ws.numel(), D.stream(self.device)),
               "smpc_finish")
@@ -664,7 +690,8 @@ class SmpcSession:
 
     def launch(self) -> None:
         """Replay the step graph asynchronously with the last staged inputs
-        (device-side timing); the result is read by the next ``step``."""
+        (device-side timing, no result).  The next ``step`` or ``launch`` waits
+        for this replay before it restages the inputs."""
         check(self._lib.vpb_smpc_session_launch(self._h, D.stream(self.pl.device)), "smpc_session_launch")
 
     def close(self) -> None:
