@@ -185,25 +185,16 @@ def closed_loop(dev, dims, samples, horizon, frames, warm=3):
     from paper_2512_22575_b200 import config, mapping, planner, robot, scene
 
     chain, model = config.robot_7dof()
-    n = len(dims)
     grid, cam, _ = scene.bench_edt_scene(dims, device=dev)
     mapper = mapping.OccupancyMapper(grid, cam, outside_default=0.8)
-    extent = np.array(dims) * grid.voxel_size
     params = config.planner_params(7, {"samples": samples, "horizon": horizon})
     pl = planner.Planner(chain, model, params, device=dev)
     state = robot.JointState.resting(np.full(7, 0.05))
     goal = robot.forward_kinematics(chain, np.full(7, 0.35))[-1]
     nominal = np.zeros((horizon, 7))
-    half = np.maximum(extent * 0.25, grid.voxel_size * 2) / 2.0
-    center = np.array([0.0, 0.0, extent[2] * 0.5])
-    depths, masks = [], []
-    for f in range(frames + warm):  # untimed inputs: a 10 cm cube sweeping past the static box
-        s_ = -1.0 + 2.0 * (f % 50) / 49.0
-        cube_c = np.array([0.4 * s_, 0.25, 0.45])
-        boxes = [(center - half, center + half), (cube_c - 0.05, cube_c + 0.05)]
-        centers, radii = robot.sphere_positions(chain, np.full(7, 0.3) + 0.01 * f, model)
-        depths.append(mapping.DepthImage(scene.render_boxes(cam, boxes, (centers, radii))))
-        masks.append((centers, radii))
+    seq = scene.moving_obstacle_frames(cam, dims, frames + warm, chain, model)
+    depths = [mapping.DepthImage(d) for d, _ in seq]
+    masks = [m for _, m in seq]
     stream = torch.cuda.current_stream(dev)
     times = []
     for f in range(frames + warm):
@@ -219,7 +210,6 @@ def closed_loop(dev, dims, samples, horizon, frames, warm=3):
             times.append(e0.elapsed_time(e1))
         state = pl.integrate(state, res.command)
         nominal = res.next_nominal
-    del n
     return {"metric": "p50 replan ms", "value": statistics.median(times), "unit": "ms",
             "p90": float(np.percentile(times, 90)), "frames": frames, "grid": list(dims), "samples": samples,
             "horizon": horizon,

@@ -110,3 +110,28 @@ REACH_STATIC_START = np.array([0.6, 1.0, 0.0, -0.9, 0.0, 0.7, 0.0])
 REACH_STATIC_GOAL = [0.3776841587, -0.2583876349, 0.8979771853, 0.8799231763, 0.1150809890, 0.3720255519,
                      -0.2721921353]
 REACH_STATIC_QREF = [0.0, 0.95, 0.0, -0.85, 0.0, 0.72, 0.0]
+
+
+def moving_obstacle_frames(cam: CameraModel, dims, frames: int, chain=None, model=None):
+    """Depth frames + body masks of the closed-loop scene:
+    the CLI bench box plus a 10 cm cube sweeping past it like the MotionScript
+    of vp/data/two_goal_dynamic.yaml:33-41, the 7-DoF body rendered at a
+    slowly moving configuration.  Host render (untimed input generation).
+    Returns a list of (depth (H, W) f64, (centers, radii))."""
+    from . import config, robot
+
+    if chain is None:
+        chain, model = config.robot_7dof()
+    dims = tuple(int(d) for d in dims)
+    voxel = 0.02
+    extent = np.array(dims) * voxel
+    half = np.maximum(extent * 0.25, voxel * 2) / 2.0
+    center = np.array([0.0, 0.0, extent[2] * 0.5])
+    out = []
+    for f in range(frames):
+        s_ = -1.0 + 2.0 * (f % 50) / 49.0
+        cube_c = np.array([0.4 * s_, 0.25, 0.45])
+        boxes = [(center - half, center + half), (cube_c - 0.05, cube_c + 0.05)]
+        centers, radii = robot.sphere_positions(chain, np.full(7, 0.3) + 0.01 * f, model)
+        out.append((render_boxes(cam, boxes, (centers, radii)), (centers, radii)))
+    return out

@@ -3,7 +3,7 @@
 Run in the build container only (the reference does not exist on the GPU box):
 
     PYTHONPATH=/root/reference/pkg/src NUMBA_CACHE_DIR=/tmp/numba_cache \
-        python tests/golden/make_golden.py
+        python tests/golden/make_golden.py [name,name,...]
 
 Every case below is built from the reference's own tests, CLI bench scenes and
 acceptance scenes (file:line cited per case) and stores both the inputs and the
@@ -17,6 +17,8 @@ Outputs (compressed npz, a few MB in total):
   query.npz     _query_metric probes (vp/mapping.py:616-710)
   rollout.npz   evaluate_batch cases with all 49 packed args (vp/batch.py:161-336)
   softmin.npz   soft_weights / update_controls / smpc_step (vp/planner.py:373-630)
+  edt_acceptance.npz  all 100 grids of acceptance criterion 1 (t/test_acceptance.py:57-81)
+  integrate.npz Planner.integrate sequences (vp/planner.py:632-636)
 """
 
 from __future__ import annotations
@@ -499,9 +501,62 @@ def make_softmin() -> dict:
     return d
 
 
+# --------------------------------------------------------------------------
+# EDT acceptance criterion 1 (all 100 grids) and Planner.integrate
+# --------------------------------------------------------------------------
+def make_edt_acceptance() -> dict:
+    """t/test_acceptance.py:57-81: 100 random 16^3 grids in the test's own RNG
+    order (density ~ U(0.01, 0.5), then the occupancy draw)."""
+    d: dict[str, np.ndarray] = {}
+    rng = np.random.default_rng(20240817)
+    occs, sqs = [], []
+    for _ in range(100):
+        dims = (16, 16, 16)
+        grid = VoxelGrid((0.0, 0.0, 0.0), 0.1, dims)
+        density = rng.uniform(0.01, 0.5)
+        occ = rng.random(dims) < density
+        grid.log_odds[occ] = grid.params.l_max
+        occs.append(np.packbits(occ.reshape(-1)))
+        sqs.append(sq_to_i32(edt_3d(grid).sq))
+    d["occ"] = np.stack(occs)
+    d["sq"] = np.stack(sqs)
+    return d
+
+
+def make_integrate() -> dict:
+    """Planner.integrate (vp/planner.py:632-636) on seeded states/commands."""
+    chain, model = load_robot(config.bundled_scenario_path("robot_7dof"))
+    rng = np.random.default_rng(632)
+    d: dict[str, np.ndarray] = {}
+    for j, dt_rate in enumerate((None, 100.0, 250.0)):
+        over = {} if dt_rate is None else {"dt": 1.0 / dt_rate}
+        params = config.planner_params(7, over)
+        planner = Planner(chain, model, params)
+        q, qd = rng.uniform(-1, 1, 7), rng.uniform(-0.5, 0.5, 7)
+        state = JointState(q, qd, np.zeros(7))
+        qs, qds, accs, cmds = [], [], [], []
+        for _ in range(20):
+            cmd = rng.uniform(-3, 3, 7)
+            state = planner.integrate(state, cmd)
+            cmds.append(cmd)
+            qs.append(state.q)
+            qds.append(state.qd)
+            accs.append(state.qdd)
+        d[f"i_dt_{j}"] = np.array(params.dt)
+        d[f"i_q0_{j}"], d[f"i_qd0_{j}"] = q, qd
+        d[f"i_cmd_{j}"], d[f"i_q_{j}"] = np.array(cmds), np.array(qs)
+        d[f"i_qd_{j}"], d[f"i_qdd_{j}"] = np.array(qds), np.array(accs)
+    d["i_count"] = np.array(3)
+    return d
+
+
 def main():
+    only = set(sys.argv[1].split(",")) if len(sys.argv) > 1 else None
     for name, fn in (("edt", make_edt), ("fusion", make_fusion), ("query", make_query),
-                     ("rollout", make_rollout), ("softmin", make_softmin)):
+                     ("rollout", make_rollout), ("softmin", make_softmin),
+                     ("edt_acceptance", make_edt_acceptance), ("integrate", make_integrate)):
+        if only is not None and name not in only:
+            continue
         data = fn()
         path = OUT / f"{name}.npz"
         np.savez_compressed(path, **data)

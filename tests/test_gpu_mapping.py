@@ -119,6 +119,51 @@ def test_edt_512_properties(M):
     assert bool((b <= a).all())
 
 
+def test_edt_acceptance_100_grids(M):
+    """All 100 grids of acceptance criterion 1 (t/test_acceptance.py:57-81),
+    against the reference's own outputs (tests/golden/edt_acceptance.npz)."""
+    g = load_golden("edt_acceptance")
+    for i in range(g["occ"].shape[0]):
+        occ = unpack_occ(g["occ"][i], (16, 16, 16))
+        np.testing.assert_array_equal(M.edt_3d(grid_from_occ(M, occ)).sq, i32_to_sq(g["sq"][i]), err_msg=f"grid {i}")
+
+
+@pytest.mark.parametrize("dims,density,seed", [
+    ((600, 40, 32), 0.002, 21),   # x > 512: the 64-bit (WIDE) X pass
+    ((40, 600, 32), 0.002, 22),   # y > 512: the 64-bit (WIDE) Z+Y pass
+    ((24, 24, 1100), 0.001, 23),  # z > 1024: bit-scan Z pass + the generic FH passes
+    ((1100, 8, 8), 0.002, 24),    # x > 1024: the generic (non-tiled) FH pass
+    ((8, 1100, 8), 0.002, 25),    # y > 1024
+    ((600, 40, 30), 0.003, 26),   # z % 4 != 0 with x > 512: the tile-per-line fallback
+    ((1030, 3, 5), 0.0, 27),      # empty, long
+])
+def test_edt_long_lines_vs_oracle(M, dims, density, seed):
+    occ = np.random.default_rng(seed).random(dims) < density
+    if density > 0:
+        occ[0, 0, 0] = occ[-1, -1, -1] = True  # sources at both ends of the longest lines
+    got = M.edt_3d(grid_from_occ(M, occ)).sq
+    oracle.set_threads(0)
+    np.testing.assert_array_equal(got, oracle.edt3d_from_occupancy(occ))
+
+
+@pytest.mark.parametrize("density", [0.001, 0.1, 0.5])
+def test_edt_512_random_vs_oracle(M, density):
+    """C5 size, bit-exact against the oracle over the whole 512^3 field."""
+    occ = np.random.default_rng(512).random((512, 512, 512), dtype=np.float32) < density
+    got = M.edt_3d(grid_from_occ(M, occ)).sq_device.cpu().numpy()
+    oracle.set_threads(0)
+    want = oracle.edt3d_from_occupancy(occ)
+    assert np.array_equal(got.astype(np.float64), want)
+
+
+@pytest.mark.parametrize("density", [0.1, 0.5])
+def test_edt_256_densities_vs_oracle(M, density):
+    occ = np.random.default_rng(256).random((256, 256, 256)) < density
+    got = M.edt_3d(grid_from_occ(M, occ)).sq
+    oracle.set_threads(0)
+    np.testing.assert_array_equal(got, oracle.edt3d_from_occupancy(occ))
+
+
 # ----------------------------------------------------------------------------- fusion
 def _camera(M, g, i):
     from paper_2512_22575_b200.geometry import RigidTransform, Rotation3
@@ -308,3 +353,30 @@ def test_fusion_prefilter_stress_vs_oracle(M):
         np.testing.assert_array_equal(grid.log_odds_host(), lo, err_msg=f"camera {i}")
         np.testing.assert_array_equal(grid.observed_host(), ob, err_msg=f"camera {i}")
     assert ob.sum() > 1000
+
+
+def test_mapper_pipeline_512_c5_frames(M):
+    """C5 map path (512^3 bench grid, moving cube, 7-DoF body mask), 3
+    frames: log_odds / observed bitwise and the EDT bit-exact against the
+    oracle after every frame.  At 512^3 the coordinates are largest, which
+    is where the fp32 prefilter's error bounds matter most."""
+    from paper_2512_22575_b200 import scene
+
+    grid, cam, _ = scene.bench_edt_scene((512, 512, 512))
+    mapper = M.OccupancyMapper(grid, cam, outside_default=0.8)
+    lo = np.zeros(grid.dims)
+    ob = np.zeros(grid.dims, bool)
+    r, t = cam.world_to_camera()
+    oracle.set_threads(0)
+    for f, (depth, (centers, radii)) in enumerate(scene.moving_obstacle_frames(cam, grid.dims, 3)):
+        mapper.update(M.DepthImage(depth), mask=(centers, radii))
+        pm = oracle.masked_pixels(depth, cam.fx, cam.fy, cam.cx, cam.cy, cam.d_min, cam.d_max,
+                                  cam.pose.rotation.matrix, cam.pose.translation, centers, radii, 0.01)
+        oracle.fuse_voxels(lo, ob, (0, 0, 0), grid.dims, grid.origin, grid.voxel_size, r, t, cam.fx, cam.fy,
+                           cam.cx, cam.cy, cam.width, cam.height, cam.d_min, cam.d_max, depth, pm, centers,
+                           radii, grid.tau, 0.85, -0.4, -2.0, 3.5)
+        assert np.array_equal(grid.log_odds_host(), lo), f"frame {f}: log_odds"
+        assert np.array_equal(grid.observed_host(), ob), f"frame {f}: observed"
+        field = mapper.recompute_edt()
+        assert np.array_equal(field.sq_device.cpu().numpy().astype(np.float64), oracle.edt3d(lo)), f"frame {f}: EDT"
+    assert ob.sum() > 100000

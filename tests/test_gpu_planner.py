@@ -589,3 +589,21 @@ def test_sharded_graph_nccl_world1_equals_step(pk):
             np.testing.assert_allclose(got.diagnostics.weighted_cost, want.diagnostics.weighted_cost, rtol=1e-12)
     finally:
         dist.destroy_process_group()
+
+
+def test_integrate_matches_reference_golden(pk):
+    """Planner.integrate (vp/planner.py:632-636) against the reference's own
+    outputs (tests/golden/integrate.npz): bitwise, the same two fp64
+    multiply-adds in the same order."""
+    pkg, config, mapping, planner, robot = pk
+    g = load_golden("integrate")
+    chain, model = config.robot_7dof()
+    for j in range(int(g["i_count"])):
+        params = config.planner_params(7, {"dt": float(g[f"i_dt_{j}"])})
+        pl = planner.Planner(chain, model, params)
+        state = robot.JointState(g[f"i_q0_{j}"], g[f"i_qd0_{j}"], np.zeros(7))
+        for k, cmd in enumerate(g[f"i_cmd_{j}"]):
+            state = pl.integrate(state, cmd)
+            np.testing.assert_array_equal(state.q, g[f"i_q_{j}"][k])
+            np.testing.assert_array_equal(state.qd, g[f"i_qd_{j}"][k])
+            np.testing.assert_array_equal(state.qdd, g[f"i_qdd_{j}"][k])

@@ -178,3 +178,49 @@ def test_golden_fields_are_lipschitz_edts():
             assert np.isinf(d).all()  # no source at all
         i += 1
     assert checked >= 1
+
+
+def brute_force_sqdist(occ):
+    """Independent O(N * sources) check, as vp/oracles.py:68-101 does for
+    acceptance criterion 1 (t/test_acceptance.py:57-81)."""
+    src = np.argwhere(occ)
+    out = np.full(occ.shape, np.inf)
+    if len(src):
+        idx = np.indices(occ.shape).reshape(3, -1).T
+        d = ((idx[:, None, :] - src[None, :, :]) ** 2).sum(-1).min(1)
+        out = d.reshape(occ.shape).astype(float)
+    return out
+
+
+def test_edt_acceptance_100_grids_golden():
+    """All 100 grids of acceptance criterion 1: oracle == reference == brute force."""
+    g = load_golden("edt_acceptance")
+    for i in range(g["occ"].shape[0]):
+        occ = unpack_occ(g["occ"][i], (16, 16, 16))
+        want = i32_to_sq(g["sq"][i])
+        np.testing.assert_array_equal(want, brute_force_sqdist(occ), err_msg=f"grid {i}: golden vs brute force")
+        np.testing.assert_array_equal(oracle.edt3d_from_occupancy(occ), want, err_msg=f"grid {i}")
+
+
+def test_reference_arm_scene_matches_product_mirror():
+    """oracle/scene.py (the reference arm's host-only scene, no product import)
+    builds the same problem as the product's host mirror."""
+    from oracle import scene as osc
+    from paper_2512_22575_b200 import config, planner, robot
+    from conftest import oracle_args
+
+    chain, model = config.robot_7dof()
+    params = config.planner_params(7, {"samples": 4096, "horizon": 32})
+    state = robot.JointState.resting(np.full(7, 0.05))
+    goal = robot.forward_kinematics(chain, np.full(7, 0.35))[-1]
+    want = oracle_args(planner, chain, model, params, state, goal, None)
+    got = osc.rollout_args(np.zeros((1, 1, 1)), np.zeros(3), 1.0)
+    for k, v in want.items():
+        if k.startswith("field_"):
+            continue
+        np.testing.assert_allclose(np.asarray(got[k], float), np.asarray(v, float), rtol=0, atol=1e-15, err_msg=k)
+    c0, r0 = robot.sphere_positions(chain, np.full(7, 0.3), model)
+    c1, r1 = osc.sphere_positions(np.full(7, 0.3))
+    np.testing.assert_allclose(c1, c0, rtol=0, atol=1e-15)
+    np.testing.assert_array_equal(r1, r0)
+    assert params.lam == osc.DEFAULTS["lam"] and params.noise_window == osc.DEFAULTS["noise_window"]
