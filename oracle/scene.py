@@ -171,3 +171,23 @@ def rollout_args(sq, origin, voxel, outside=0.8, q0=0.05, q_goal=0.35, q_ref=Non
                     tightened_limits(DEFAULTS["margin_frac"])):
         args[k] = v
     return args
+
+
+def moving_obstacle_frames(dims, frames: int):
+    """Host copy of the closed-loop input sequence (the product's
+    scene.moving_obstacle_frames): the bench box plus a
+    10 cm cube sweeping along x, the body at q = 0.3 + 0.01 f.
+    Returns [(depth, (centers, radii))]."""
+    voxel = 0.02
+    extent = np.array(dims) * voxel
+    half = np.maximum(extent * 0.25, voxel * 2) / 2.0
+    center = np.array([0.0, 0.0, extent[2] * 0.5])
+    cam = Camera()
+    out = []
+    for f in range(frames):
+        s_ = -1.0 + 2.0 * (f % 50) / 49.0
+        cube_c = np.array([0.4 * s_, 0.25, 0.45])
+        spheres = sphere_positions(np.full(7, 0.3) + 0.01 * f)
+        out.append((render_boxes(cam, [(center - half, center + half), (cube_c - 0.05, cube_c + 0.05)], spheres),
+                    spheres))
+    return out
