@@ -15,6 +15,9 @@
 // integer cross-multiplications of the parabola intersections (exact; no
 // division), with only finite sources ever entering the envelope.
 #include <climits>
+#include <cstdlib>
+
+#include <cuda.h>
 
 #include "vpb_common.cuh"
 
@@ -248,67 +251,6 @@ __global__ void __launch_bounds__(64) edt_pass_fh(const TIn *__restrict__ in, TO
 }
 
 // ---------------------------------------------------------------------------
-// Fast z pass (box z-length <= 1024): one warp per (x, y) line.  Lane i holds
-// the i-th 32-bit word of the line's occupancy; a warp max-scan / min-scan
-// over the words gives every word the last source before it and the first
-// source after it, so each output needs one word and two shuffled carries.
-// Writes u16 nearest-source distances (0xFFFF = no source on the line).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) edt_pass_z_scan(const uint32_t *__restrict__ bits, int64_t gy,
-                                                       int64_t words_z, int64_t lo0, int64_t lo1, int lo2,
-                                                       int64_t n0, int64_t n1, int n2, uint16_t *__restrict__ out) {
-  const int lane = threadIdx.x & 31;
-  // grid: (ceil(n1 / 8), n0)
-  const int64_t i1 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (i1 >= n1) return;
-  const int64_t i0 = blockIdx.y;
-  const int64_t line = i0 * n1 + i1;
-  const uint32_t *w = bits + ((lo0 + i0) * gy + (lo1 + i1)) * words_z;
-  const int nw = (n2 + 31) >> 5;
-  uint32_t word = 0;
-  if (lane < nw) {
-    const int zb = lo2 + 32 * lane;  // global z of bit 0 of this window
-    const int wi = zb >> 5, sh = zb & 31;
-    const uint32_t a = __ldg(w + wi);
-    const uint32_t b = (sh != 0 && wi + 1 < words_z) ? __ldg(w + wi + 1) : 0u;
-    word = sh ? __funnelshift_r(a, b, sh) : a;
-    const int valid = n2 - 32 * lane;
-    if (valid < 32) word &= (1u << valid) - 1u;
-  }
-  // last source at or before each word / first source at or after it
-  int last = word ? 32 * lane + 31 - __clz(word) : -1;
-  int first = word ? 32 * lane + __ffs(word) - 1 : 0x7fffffff;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int l = __shfl_up_sync(kFull, last, d);
-    if (lane >= d) last = max(last, l);
-    const int f = __shfl_down_sync(kFull, first, d);
-    if (lane + d < 32) first = min(first, f);
-  }
-  // exclusive versions: before word i / after word i
-  int last_ex = __shfl_up_sync(kFull, last, 1);
-  if (lane == 0) last_ex = -1;
-  int first_ex = __shfl_down_sync(kFull, first, 1);
-  if (lane == 31) first_ex = 0x7fffffff;
-  uint16_t *o = out + line * n2;
-  const uint32_t le_mask = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
-  const uint32_t ge_mask = 0xffffffffu << lane;
-  for (int c = 0; c < nw; ++c) {
-    const uint32_t wc = __shfl_sync(kFull, word, c);
-    const int lx = __shfl_sync(kFull, last_ex, c);
-    const int fx = __shfl_sync(kFull, first_ex, c);
-    const int z = 32 * c + lane;
-    const uint32_t le = wc & le_mask, ge = wc & ge_mask;
-    const int left = le ? 32 * c + 31 - __clz(le) : lx;
-    const int right = ge ? 32 * c + __ffs(ge) - 1 : fx;
-    int d = 0x7fffffff;
-    if (left >= 0) d = z - left;
-    if (right != 0x7fffffff) d = min(d, right - z);
-    if (z < n2) o[z] = d == 0x7fffffff ? kNoSrc16 : (uint16_t)min(d, 0xFFFE);
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Shared-memory FH pass.  A 32-thread CTA owns 32 lines (lanes over the
 // contiguous z axis), stages them as a [len][32] u32 tile (coalesced loads,
 // conflict-free column access), runs the lower-envelope sweep per lane and
@@ -446,38 +388,56 @@ static int launch_fh_smem(const TIn *in, TOut *out, int64_t n_outer, int64_t out
 // ---------------------------------------------------------------------------
 // Segmented FH line kernels (the production path for lines <= 1024).
 //
-// A 128-thread CTA owns 32 lines (lanes over the contiguous z axis) staged as
-// a [len][32] u32 tile in shared memory.  Each line is split into KSEG = 4
-// segments handled by 4 threads: each builds the lower envelope of its
-// segment in place (stack entry (f << 10) | v over consumed input slots),
-// the envelopes are merged pairwise (the merged envelope of two runs is a
-// prefix of the left run plus a suffix of the right one, found by dropping
-// boundary parabolas that are dominated by their neighbours), and every
-// thread then locates the parabola covering its first output by binary
-// search and sweeps its segment.  Tile columns are rotated by 8 per segment
-// so the 4 threads of a line hit different banks.
+// A 128-thread CTA owns 32 lines (lane = line, over the contiguous z axis)
+// staged as a [len][32] u32 tile in shared memory (row q = element q of the
+// 32 lines; a warp reads one 128 B row, conflict-free).  Each line is split
+// into KSEG = 4 segments, segment = warp: every thread builds the lower
+// envelope of its segment IN PLACE (stack entry k overwrites tile row
+// q0 + k, whose input is already consumed; entry = (F << 10) | v with
+// F = f + v^2 < 2^22), the runs are merged pairwise (the envelope of two runs
+// is a prefix of the left run plus a suffix of the right one: drop boundary
+// parabolas dominated by their neighbours), then every thread locates the
+// parabola covering its first output by binary search and sweeps its
+// segment run-length: the envelope switches from c to n at the integer
+// q_sw = floor((F_n - F_c) / 2 (v_n - v_c)) + 1, computed with one
+// approximate fp32 division and an exact integer correction (no 64-bit
+// division), so a run of outputs costs one multiply-add and one store each.
+// Every comparison is exact integer arithmetic, so the result equals the
+// reference's f64 FH (vp/mapping.py:458-483) bit for bit.
 // ---------------------------------------------------------------------------
 constexpr int KSEG = 4;
-constexpr int LINES = 32;
-constexpr int ETHREADS = LINES * KSEG;
+constexpr int ETHREADS = 32 * KSEG;
 
 struct SegLine {
   int lo[KSEG], hi[KSEG];
 };
 
-__device__ __forceinline__ int tslot(int line, int seg, int row) { return row * 32 + ((line + 8 * seg) & 31); }
-
 struct Elem {
-  int v, f, F;
+  int v, F;  // F = f + v^2
 };
 
-__device__ __forceinline__ Elem elem_at(const uint32_t *tile, int line, int B, int seg, int idx) {
-  const uint32_t e = tile[tslot(line, seg, seg * B + idx)];
+// Shared-memory accesses by explicit 32-bit shared-window address (the
+// generic-pointer form made the compiler re-derive the window base from
+// SR_CgaCtaId on every access inside the envelope loops).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v));
+}
+
+__device__ __forceinline__ Elem unpack_entry(uint32_t e) {
   Elem r;
   r.v = (int)(e & 1023u);
-  r.f = (int)(e >> 10);
-  r.F = r.f + r.v * r.v;
+  r.F = (int)(e >> 10);
   return r;
+}
+
+// column address of (row r) for this thread: col + r * 128
+__device__ __forceinline__ Elem elem_at(uint32_t col, int B, int seg, int idx) {
+  return unpack_entry(lds_u32(col + (uint32_t)(seg * B + idx) * 128u));
 }
 
 // s(a, b) < q  <=>  F_b - F_a < 2 q (v_b - v_a).  WIDE: 64-bit products
@@ -528,7 +488,7 @@ __device__ __forceinline__ bool next_elem(const SegLine &S, int seg, int idx, in
 
 // Merge left run (segments a..b) with right run (b+1..c) of one line.
 template <bool WIDE>
-__device__ void merge_runs(const uint32_t *tile, int line, int B, SegLine &S, int a, int b, int c) {
+__device__ void merge_runs(uint32_t col, int B, SegLine &S, int a, int b, int c) {
   int ls = -1, li = 0, rs = -1, ri = 0;
   for (int t = b; t >= a; --t)
     if (S.hi[t] > S.lo[t]) {
@@ -545,11 +505,11 @@ __device__ void merge_runs(const uint32_t *tile, int line, int B, SegLine &S, in
   if (ls < 0 || rs < 0) return;
   while (true) {
     bool changed = false;
-    const Elem L1 = elem_at(tile, line, B, ls, li);
-    const Elem R1 = elem_at(tile, line, B, rs, ri);
+    const Elem L1 = elem_at(col, B, ls, li);
+    const Elem R1 = elem_at(col, B, rs, ri);
     int ps, pi;
     if (prev_elem(S, ls, li, a, ps, pi)) {
-      const Elem L2 = elem_at(tile, line, B, ps, pi);
+      const Elem L2 = elem_at(col, B, ps, pi);
       if (dominated<WIDE>(L2, L1, R1)) {
         S.hi[ls] = li;  // drop the left run's last element
         ls = ps;
@@ -560,7 +520,7 @@ __device__ void merge_runs(const uint32_t *tile, int line, int B, SegLine &S, in
     if (!changed) {
       int ns, ni;
       if (next_elem(S, rs, ri, c, ns, ni)) {
-        const Elem R2 = elem_at(tile, line, B, ns, ni);
+        const Elem R2 = elem_at(col, B, ns, ni);
         if (dominated<WIDE>(L1, R1, R2)) {
           S.lo[rs] = ri + 1;  // drop the right run's first element
           rs = ns;
@@ -577,312 +537,358 @@ template <typename TOut>
 __device__ __forceinline__ void store_dist(TOut *p, int v);
 template <>
 __device__ __forceinline__ void store_dist<int32_t>(int32_t *p, int v) {
-  *p = v < 0 ? -1 : v;  // -1 = no source: the X pass copies it raw (== kTileInf)
+  *p = v;  // -1 = no source: the X pass stages it raw (== kTileInf)
 }
 template <>
 __device__ __forceinline__ void store_dist<float>(float *p, int v) {
   *p = v < 0 ? __int_as_float(0x7f800000) : (float)v;
 }
 
-// Envelope + output for the tile (called by all ETHREADS threads after the
-// tile is filled and synchronised).  dst_base + line + q * stride receives
-// output q of `line`.
+// Forward sweep of one thread's segment [q0, q1): lower envelope of the finite
+// parabolas, stack IN PLACE at column rows q0 + k (entry (F << 10) | v).
+// `State` carries the top two entries in registers.
+struct FwdState {
+  int k, vt, vp, Ft, Fp;
+};
+
+template <bool WIDE>
+__device__ __forceinline__ void fwd_step(FwdState &S, uint32_t stk, int q, uint32_t e) {
+  if (e == kTileInf) return;
+  const int Fq = (int)e + q * q;
+  while (S.k >= 1) {
+    const bool pop = WIDE ? ((long long)(Fq - S.Ft) * (S.vt - S.vp) <= (long long)(S.Ft - S.Fp) * (q - S.vt))
+                          : ((Fq - S.Ft) * (S.vt - S.vp) <= (S.Ft - S.Fp) * (q - S.vt));
+    if (!pop) break;
+    --S.k;
+    S.vt = S.vp;
+    S.Ft = S.Fp;
+    if (S.k >= 1) {
+      const Elem p = unpack_entry(lds_u32(stk + 128u * (uint32_t)(S.k - 1)));
+      S.vp = p.v;
+      S.Fp = p.F;
+    }
+  }
+  ++S.k;
+  sts_u32(stk + 128u * (uint32_t)S.k, ((uint32_t)Fq << 10) | (uint32_t)q);
+  S.vp = S.vt;
+  S.Fp = S.Ft;
+  S.vt = q;
+  S.Ft = Fq;
+}
+
+// Merges of the 4 segment runs + output sweep (all ETHREADS threads; no early
+// return, so it can sit inside a persistent loop).  `k` = this thread's stack
+// top from the forward sweep.  dst_base[line + q * stride] receives output q.
 template <typename TOut, bool WIDE>
-__device__ void segmented_fh(uint32_t *tile, SegLine *segs, int len, int nlines_active, TOut *dst_base,
-                             int64_t stride) {
+__device__ __forceinline__ void fh_merge_output(uint32_t tile_s, SegLine *segs, int len, bool act, int k,
+                                                TOut *__restrict__ dst_base, uint32_t stride) {
   const int tid = threadIdx.x;
   const int s = tid >> 5;     // segment = warp index
   const int line = tid & 31;  // z lane
   const int B = (len + KSEG - 1) / KSEG;
   const int q0 = s * B, q1 = min(len, q0 + B);
-  const bool act = line < nlines_active;
-  uint32_t *col = tile + ((line + 8 * s) & 31);  // this thread's column; row r at col[r * 32]
-  // ---- forward sweep on this segment (stack in place) ----
-  int k = -1;
-  if (act) {
-    int vt = 0, vp = 0, Ft = 0, Fp = 0;
-    const uint32_t *src = col + q0 * 32;
-    for (int q = q0; q < q1; ++q, src += 32) {
-      const uint32_t e = *src;
-      if (e == kTileInf) continue;
-      const int fq = (int)e;
-      const int Fq = fq + q * q;
-      while (k >= 1) {
-        const bool pop = WIDE ? ((long long)(Fq - Ft) * (vt - vp) <= (long long)(Ft - Fp) * (q - vt))
-                              : ((Fq - Ft) * (vt - vp) <= (Ft - Fp) * (q - vt));
-        if (!pop) break;
-        --k;
-        vt = vp;
-        Ft = Fp;
-        if (k >= 1) {
-          const uint32_t se = col[(q0 + k - 1) * 32];
-          vp = (int)(se & 1023u);
-          Fp = (int)(se >> 10) + vp * vp;
-        }
-      }
-      ++k;
-      col[(q0 + k) * 32] = ((uint32_t)fq << 10) | (uint32_t)q;
-      vp = vt;
-      Fp = Ft;
-      vt = q;
-      Ft = Fq;
-    }
-  }
+  const uint32_t col = tile_s + 4u * (uint32_t)line;
   segs[line].lo[s] = 0;
   segs[line].hi[s] = k + 1;
   __syncthreads();
   // ---- merges: (0,1) and (2,3), then (01, 23) ----
-  if (act && (s == 0 || s == 2)) merge_runs<WIDE>(tile, line, B, segs[line], s, s, s + 1);
+  if (act && (s == 0 || s == 2)) merge_runs<WIDE>(col, B, segs[line], s, s, s + 1);
   __syncthreads();
-  if (act && s == 0) merge_runs<WIDE>(tile, line, B, segs[line], 0, 1, 3);
+  if (act && s == 0) merge_runs<WIDE>(col, B, segs[line], 0, 1, 3);
   __syncthreads();
-  if (!act || q0 >= q1) return;
-  // segment bounds of the merged envelope in registers (indexed only through
-  // unrolled selects: no local memory)
-  int lo_[KSEG], hi_[KSEG];
-#pragma unroll
-  for (int t = 0; t < KSEG; ++t) {
-    lo_[t] = segs[line].lo[t];
-    hi_[t] = segs[line].hi[t];
-  }
-  auto sel = [&](const int (&a)[KSEG], int t) {
-    int v = a[0];
-#pragma unroll
-    for (int u = 1; u < KSEG; ++u) v = t == u ? a[u] : v;
-    return v;
-  };
-  int total = 0;
-#pragma unroll
-  for (int t = 0; t < KSEG; ++t) total += hi_[t] - lo_[t];
-  TOut *dst = dst_base + line + (int64_t)q0 * stride;
-  if (total == 0) {
-    for (int q = q0; q < q1; ++q, dst += stride) store_dist<TOut>(dst, -1);
-    return;
-  }
-  auto rank_to = [&](int r, int &sg, int &ix) {
-    sg = KSEG - 1;
-    ix = hi_[KSEG - 1] - 1;
-    bool found = false;
+  if (act && q0 < q1) {
+    // segment bounds of the merged envelope in registers (indexed only
+    // through unrolled selects: no local memory)
+    int lo_[KSEG], hi_[KSEG];
 #pragma unroll
     for (int t = 0; t < KSEG; ++t) {
-      const int sz = hi_[t] - lo_[t];
-      if (!found && r < sz) {
-        sg = t;
-        ix = lo_[t] + r;
-        found = true;
-      }
-      if (!found) r -= sz;
+      lo_[t] = segs[line].lo[t];
+      hi_[t] = segs[line].hi[t];
     }
-  };
-  auto elem = [&](int sg, int ix) { return elem_at(tile, line, B, sg, ix); };
-  // largest r with r == 0 or s(e_{r-1}, e_r) < q0
-  int lo = 0, hi = total - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    int sa, ia, sb, ib;
-    rank_to(mid - 1, sa, ia);
-    rank_to(mid, sb, ib);
-    if (boundary_lt<WIDE>(elem(sa, ia), elem(sb, ib), q0))
-      lo = mid;
-    else
-      hi = mid - 1;
-  }
-  int cs, ci;
-  rank_to(lo, cs, ci);
-  int rk = lo;  // rank of cur
-  Elem cur = elem(cs, ci);
-  // next element: same segment, else the next non-empty one
-  auto step = [&](int &sg, int &ix) {
-    if (ix + 1 < sel(hi_, sg)) {
-      ++ix;
-      return;
-    }
-    int ns = sg, ni = ix;
+    int total = 0;
 #pragma unroll
-    for (int t = KSEG - 1; t >= 1; --t)
-      if (t > sg && hi_[t] > lo_[t]) {
-        ns = t;
-        ni = lo_[t];
+    for (int t = 0; t < KSEG; ++t) total += hi_[t] - lo_[t];
+    uint32_t off = (uint32_t)line + (uint32_t)q0 * stride;
+    if (total == 0) {
+      for (int q = q0; q < q1; ++q, off += stride) store_dist<TOut>(dst_base + off, -1);
+    } else {
+      auto rank_to = [&](int r, int &sg, int &ix) {
+        sg = KSEG - 1;
+        ix = hi_[KSEG - 1] - 1;
+        bool found = false;
+#pragma unroll
+        for (int t = 0; t < KSEG; ++t) {
+          const int sz = hi_[t] - lo_[t];
+          if (!found && r < sz) {
+            sg = t;
+            ix = lo_[t] + r;
+            found = true;
+          }
+          if (!found) r -= sz;
+        }
+      };
+      auto elem = [&](int sg, int ix) { return elem_at(col, B, sg, ix); };
+      // largest r with r == 0 or s(e_{r-1}, e_r) < q0
+      int lo = 0, hi = total - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        int sa, ia, sb, ib;
+        rank_to(mid - 1, sa, ia);
+        rank_to(mid, sb, ib);
+        if (boundary_lt<WIDE>(elem(sa, ia), elem(sb, ib), q0))
+          lo = mid;
+        else
+          hi = mid - 1;
       }
-    sg = ns;
-    ix = ni;
-  };
-  int ns = cs, ni = ci;
-  bool has_next = rk + 1 < total;
-  Elem nxt = cur;
-  if (has_next) {
-    step(ns, ni);
-    nxt = elem(ns, ni);
-  }
-  // The envelope changes to `nxt` at the first q with F_n - F_c < 2 q (v_n - v_c)
-  // (v_n > v_c): q_sw = floor((F_n - F_c) / (2 (v_n - v_c))) + 1.  Between
-  // switches the outputs are a run of (q - v)^2 + f.
-  auto q_switch = [&](const Elem &c, const Elem &nx) -> int {
-    const long long num = (long long)nx.F - c.F, den = 2ll * (nx.v - c.v);
-    long long fl = num / den;
-    if ((num % den != 0) && (num < 0)) --fl;  // floor for a negative numerator
-    return (int)(fl + 1);
-  };
-  int qs = has_next ? q_switch(cur, nxt) : 0x7fffffff;
-  int q = q0;
-  while (q < q1) {
-    while (q >= qs) {  // advance (possibly over several parabolas)
-      cur = nxt;
-      ++rk;
-      has_next = rk + 1 < total;
-      if (has_next) {
+      int cs, ci;
+      rank_to(lo, cs, ci);
+      int left = total - 1 - lo;  // parabolas after cur
+      Elem cur = elem(cs, ci);
+      // next element: same segment, else the next non-empty one
+      auto step = [&](int &sg, int &ix) {
+        int h = hi_[0];
+#pragma unroll
+        for (int t = 1; t < KSEG; ++t) h = sg == t ? hi_[t] : h;
+        if (ix + 1 < h) {
+          ++ix;
+          return;
+        }
+        int ns = sg, ni = ix;
+#pragma unroll
+        for (int t = KSEG - 1; t >= 1; --t)
+          if (t > sg && hi_[t] > lo_[t]) {
+            ns = t;
+            ni = lo_[t];
+          }
+        sg = ns;
+        ix = ni;
+      };
+      int ns = cs, ni = ci;
+      Elem nxt = cur;
+      if (left > 0) {
         step(ns, ni);
         nxt = elem(ns, ni);
-        qs = q_switch(cur, nxt);
-      } else {
-        qs = 0x7fffffff;
+      }
+      // Output sweep (vp/mapping.py:478-483): advance while the next
+      // parabola's intersection lies strictly left of q; d(q) = (q - v)^2 + f.
+      int f = cur.F - cur.v * cur.v;
+      for (int q = q0; q < q1; ++q, off += stride) {
+        while (left > 0 && boundary_lt<WIDE>(cur, nxt, q)) {
+          cur = nxt;
+          f = cur.F - cur.v * cur.v;
+          if (--left > 0) {
+            step(ns, ni);
+            nxt = elem(ns, ni);
+          }
+        }
+        const int d = q - cur.v;
+        store_dist<TOut>(dst_base + off, d * d + f);
       }
     }
-    const int qe = qs < q1 ? qs : q1;
-    const int v = cur.v, f = cur.f;
-    for (; q < qe; ++q, dst += stride) {
-      const int d = q - v;
-      store_dist<TOut>(dst, d * d + f);
-    }
   }
 }
 
-// Per (x, y) line of the box, per 32-z word w of the box line: the nearest
-// source strictly left of the word (box-local z + 1, 0 = none) in the low 16
-// bits and the nearest strictly right (0xFFFF = none) in the high 16 bits.
-// One thread per line; 2 MB of bits in, n0 n1 ceil(n2 / 32) words out.
-__global__ void __launch_bounds__(256) edt_line_lr_kernel(const uint32_t *__restrict__ bits, int64_t gy,
-                                                          int64_t words_z, int64_t lo0, int64_t lo1, int lo2,
-                                                          int n0, int n1, int n2, uint32_t *__restrict__ lr) {
-  const int64_t line = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (line >= (int64_t)n0 * n1) return;
-  const int64_t i0 = line / n1, i1 = line - i0 * n1;
-  const uint32_t *w = bits + ((lo0 + i0) * gy + (lo1 + i1)) * words_z;
-  const int nw = (n2 + 31) >> 5;
-  uint32_t *o = lr + line * nw;
-  // all of the line's words in flight at once (nw <= 32 on this path)
-  uint32_t m[32];
-#pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    uint32_t v = 0u;
-    if (c < nw) {
-      v = load_bits_window(w, lo2 + 32 * c, words_z);
-      const int valid = n2 - 32 * c;
-      if (valid < 32) v &= (1u << valid) - 1u;
-    }
-    m[c] = v;
-  }
-  uint32_t left[32];
-  int last = -1;
-#pragma unroll
-  for (int c = 0; c < 32; ++c) {
-    left[c] = (uint32_t)(last + 1);
-    if (m[c]) last = 32 * c + 31 - __clz(m[c]);
-  }
-  int first = 0xFFFF;
-#pragma unroll
-  for (int c = 31; c >= 0; --c) {
-    if (c < nw) o[c] = left[c] | ((uint32_t)first << 16);
-    if (m[c]) first = 32 * c + __ffs(m[c]) - 1;
-  }
-}
+// "No source on this side" markers of the z scan: far enough that
+// min(z - L, R - z) >= 0x8000 flags a line without sources.
+constexpr int kNoneLo = -0x10000;
+constexpr int kNoneHi = 0x20000;
 
-// Pass Z+Y fused: CTA = (z chunk, x).  The tile row y holds dz(x, y, z)^2 for
-// the 32 z of the chunk, computed from the packed occupancy words of line
-// (x, y): the word of the chunk gives the in-chunk neighbours, a ballot over
-// the line's non-empty words gives the nearest non-empty word on each side
-// (no z-pass intermediate).  The FH then runs along y.
-// Output: int32 g(x, y, z) = min over y' of (y - y')^2 + dz^2 (INT_MAX = none).
+// Pass Z+Y fused, persistent: work item = (z chunk, x).  Warp w owns the
+// rows of segment w.  For 32 of its rows at a time (one row per lane, all of
+// the line's occupancy words in flight at once) it resolves the chunk's own
+// 32-bit word and the nearest source on each side of the chunk; the rows are
+// then broadcast lane to lane (shuffles), every lane computes dz^2 for its z
+// and feeds it straight into the forward envelope sweep along y (no tile
+// fill pass).  Output: int32 g(x, y, z) = min over y' of (y - y')^2 + dz^2
+// (-1 = no source in the (x) plane).
 template <bool WIDE>
 __global__ void __launch_bounds__(ETHREADS) edt_zy_kernel(const uint32_t *__restrict__ bits, int64_t gy,
-                                                          int64_t words_z, int64_t lo0, int64_t lo1, int lo2,
-                                                          int n1, int n2, const uint32_t *__restrict__ lr,
+                                                          int64_t words_z, int64_t lo0, int64_t lo1, int lo2, int n0,
+                                                          int n1, int n2, int zc_base, int gz,
                                                           int32_t *__restrict__ out) {
-  extern __shared__ uint32_t smem[];
-  uint32_t *tile = smem;                                                // [n1][32]
+  extern __shared__ __align__(128) uint32_t smem[];
+  const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(smem);    // [n1][32]
   SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)n1 * 32);  // [32]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int zc = blockIdx.x;
-  const int64_t x = blockIdx.y;
   const int nw = (n2 + 31) >> 5;
-  const int nlines = min(32, n2 - zc * 32);
   const uint32_t le_mask = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
   const uint32_t ge_mask = 0xffffffffu << lane;
   const int B = (n1 + KSEG - 1) / KSEG;
-  const int z = 32 * zc + lane;
-  const int valid = n2 - 32 * zc;
-  const uint32_t vmask = valid < 32 ? (1u << valid) - 1u : 0xffffffffu;
-  const uint32_t *wbase = bits + ((lo0 + x) * gy + lo1) * words_z;
-  const uint32_t *lrbase = lr + (x * n1) * (int64_t)nw + zc;
-  uint32_t *dcol = tile + ((lane + 8 * warp) & 31);
-  // warp w fills the rows of segment w (its rotated column is warp-uniform):
-  // per row one broadcast word + one broadcast (left, right) pair
+  const bool aligned = (lo2 & 31) == 0;
   const int y0 = warp * B, y1 = min(n1, y0 + B);
-  auto fill = [&](int y, uint32_t word, uint32_t lrv) {
-    word &= vmask;
-    const uint32_t le = word & le_mask, ge = word & ge_mask;
-    const int left = le ? 32 * zc + 31 - __clz(le) : (int)(lrv & 0xFFFFu) - 1;
-    const int rgt = ge ? 32 * zc + __ffs(ge) - 1 : (int)(lrv >> 16);
-    int d = 0x7fffffff;
-    if (left >= 0) d = z - left;
-    if (rgt != 0xFFFF) d = min(d, rgt - z);
-    dcol[y * 32] = (lane < nlines && d != 0x7fffffff) ? (uint32_t)(d * d) : kTileInf;
-  };
-  int y = y0;
-  for (; y + 4 <= y1; y += 4) {
-    uint32_t wd[4], lv[4];
+  const uint32_t stk = tile_s + 4u * (uint32_t)lane + 128u * (uint32_t)y0;
+  const int items = gz * n0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x) {
+    const int zc = zc_base + item % gz;
+    const int64_t x = item / gz;
+    const int zb = 32 * zc;
+    const int nlines = min(32, n2 - zb);
+    const bool act = lane < nlines;
+    const int z = zb + lane;
+    const uint32_t *wbase = bits + ((lo0 + x) * gy + lo1) * words_z + (lo2 >> 5);
+    FwdState S{-1, 0, 0, 0, 0};
+    for (int yb = y0; yb < y1; yb += 32) {
+      // lane = row yb + lane: the chunk word and the nearest source on each side
+      const int yr = yb + lane;
+      uint32_t cw = 0;
+      int L = kNoneLo, R = kNoneHi;
+      if (yr < y1) {
+        const uint32_t *w = wbase + (int64_t)yr * words_z;
+        for (int c0 = 0; c0 < nw; c0 += 4) {
+          uint32_t m[4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      wd[t] = load_bits_window(wbase + (int64_t)(y + t) * words_z, lo2 + 32 * zc, words_z);
-      lv[t] = __ldg(lrbase + (int64_t)(y + t) * nw);
+          for (int t = 0; t < 4; ++t) {
+            const int c = c0 + t;
+            uint32_t v = 0u;
+            if (c < nw) {
+              v = aligned ? __ldg(w + c) : load_bits_window(w - (lo2 >> 5), lo2 + 32 * c, words_z);
+              const int valid = n2 - 32 * c;
+              if (valid < 32) v &= (1u << valid) - 1u;
+            }
+            m[t] = v;
+          }
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const int c = c0 + t;
+            if (m[t] && c < zc) L = 32 * c + 31 - __clz(m[t]);
+            if (c == zc) cw = m[t];
+            if (m[t] && c > zc && R == kNoneHi) R = 32 * c + __ffs(m[t]) - 1;
+          }
+        }
+      }
+      const int rows = min(32, y1 - yb);
+      for (int t = 0; t < rows; ++t) {
+        const uint32_t word = __shfl_sync(kFull, cw, t);
+        const int Lw = __shfl_sync(kFull, L, t), Rw = __shfl_sync(kFull, R, t);
+        const uint32_t le = word & le_mask, ge = word & ge_mask;
+        const int left = le ? zb + 31 - __clz(le) : Lw;
+        const int rgt = ge ? zb + __ffs(ge) - 1 : Rw;
+        const int d = min(z - left, rgt - z);
+        if (act) fwd_step<WIDE>(S, stk, yb + t, d < 0x8000 ? (uint32_t)(d * d) : kTileInf);
+      }
     }
-#pragma unroll
-    for (int t = 0; t < 4; ++t) fill(y + t, wd[t], lv[t]);
+    fh_merge_output<int32_t, WIDE>(tile_s, segs, n1, act, S.k, out + (x * n1) * (int64_t)n2 + zb, (uint32_t)n2);
+    __syncthreads();  // the tile is reused by the next item
   }
-  for (; y < y1; ++y)
-    fill(y, load_bits_window(wbase + (int64_t)y * words_z, lo2 + 32 * zc, words_z), __ldg(lrbase + (int64_t)y * nw));
-  __syncthreads();
-  int32_t *dst = out + (x * n1) * (int64_t)n2 + zc * 32;
-  segmented_fh<int32_t, WIDE>(tile, segs, n1, nlines, dst, n2);
 }
 
-// Pass X: CTA = (z chunk, y); rows x of the tile are the 32 z values of
-// g(x, y, zchunk) (one coalesced 128 B row each).
+// --- TMA helpers (cp.async.bulk.tensor + mbarrier) ---------------------------
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(a),
+      "r"(phase)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, uint64_t *bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(d),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(b)
+      : "memory");
+}
+
+constexpr int kTmaRows = 256;  // TMA box rows per copy (the box-dimension limit)
+
+// Pass X, persistent: work item = (z chunk, y).  The [n0][32] tile of
+// g(:, y, zchunk) is staged by TMA (ceil(n0 / 256) box copies of 256 rows x
+// 128 B on one mbarrier; g holds -1 == kTileInf for "no source", so the copy
+// is raw; out-of-range z lanes arrive zero-filled and stay inactive), then the
+// segmented FH runs along x and writes the f32 field.
 template <bool WIDE>
-__global__ void __launch_bounds__(ETHREADS) edt_x_kernel(const int32_t *__restrict__ g, int n0, int n1, int n2,
-                                                         float *__restrict__ out) {
-  extern __shared__ uint32_t smem[];
-  uint32_t *tile = smem;                                                // [n0][32]
-  SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)n0 * 32);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int zc = blockIdx.x;
-  const int64_t y = blockIdx.y;
-  const int nlines = min(32, n2 - zc * 32);
+__global__ void __launch_bounds__(ETHREADS) edt_x_kernel(const __grid_constant__ CUtensorMap gmap, int n0, int n1,
+                                                         int n2, int zc_base, int gz, float *__restrict__ out) {
+  extern __shared__ __align__(128) uint32_t smem[];
+  const int ncopies = (n0 + kTmaRows - 1) / kTmaRows;
+  const int rows = ncopies == 1 ? n0 : ncopies * kTmaRows;
+  uint32_t *tile = smem;                                                  // [rows][32]
+  SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)rows * 32);  // [32]
+  uint64_t *bar = reinterpret_cast<uint64_t *>(segs + 32);
+  const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
+  const int tid = threadIdx.x, lane = tid & 31, s = tid >> 5;
   const int B = (n0 + KSEG - 1) / KSEG;
-  const int64_t row_stride = (int64_t)n1 * n2;
-  const bool on = lane < nlines;
-  // Stage the [n0][32] tile with asynchronous 16-byte copies (all rows in
-  // flight at once; g holds -1 = kTileInf for "no source", so the copy is
-  // raw).  Row x lands rotated by 8 * (segment of x) words, the column
-  // layout segmented_fh expects.  Lanes past the line end are zero-filled
-  // (inactive in the envelope).
-  (void)on;
-  const int32_t *gbase = g + y * n2 + zc * 32;
-  const int bytes_row = nlines * 4;
-  for (int i = tid; i < n0 * 8; i += ETHREADS) {
-    const int r = i >> 3, piece = i & 7;  // 8 x 16 B per 128 B row
-    const int sgm = r / B;
-    const int col = (piece * 4 + 8 * sgm) & 31;
-    const int rem = bytes_row - piece * 16;
-    const int nb = rem >= 16 ? 16 : (rem > 0 ? rem : 0);
-    const int32_t *src = nb > 0 ? gbase + (int64_t)r * row_stride + piece * 4 : g;
-    const unsigned dst_s = (unsigned)__cvta_generic_to_shared(tile + r * 32 + col);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_s), "l"(src), "r"(nb) : "memory");
-  }
-  asm volatile("cp.async.wait_all;" ::: "memory");
+  const int q0 = s * B, q1 = min(n0, q0 + B);
+  const uint32_t col = tile_s + 4u * (uint32_t)lane;
+  const uint32_t stk = col + 128u * (uint32_t)q0;
+  const int box = ncopies == 1 ? n0 : kTmaRows;
+  if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
-  float *dst = out + y * n2 + zc * 32;
-  segmented_fh<float, WIDE>(tile, segs, n0, nlines, dst, row_stride);
+  const int items = gz * n1;
+  unsigned phase = 0;
+  for (int item = blockIdx.x; item < items; item += gridDim.x, phase ^= 1u) {
+    const int zc = zc_base + item % gz;
+    const int y = item / gz;
+    const int nlines = min(32, n2 - zc * 32);
+    const bool act = lane < nlines;
+    if (tid == 0) {
+      // order this CTA's earlier generic-proxy smem accesses before the async-proxy writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(bar, (unsigned)(ncopies * box * 128));
+      for (int c = 0; c < ncopies; ++c)
+        tma_load_3d(tile + (size_t)c * kTmaRows * 32, &gmap, zc * 32, y, c * kTmaRows, bar);
+    }
+    mbar_wait(bar, phase);
+    FwdState S{-1, 0, 0, 0, 0};
+    if (act && q0 < q1) {
+      uint32_t e_next = lds_u32(stk);
+      for (int q = q0; q < q1; ++q) {
+        const uint32_t e = e_next;
+        if (q + 1 < q1) e_next = lds_u32(col + 128u * (uint32_t)(q + 1));
+        fwd_step<WIDE>(S, stk, q, e);
+      }
+    }
+    fh_merge_output<float, WIDE>(tile_s, segs, n0, act, S.k, out + (int64_t)y * n2 + zc * 32, (uint32_t)(n1 * n2));
+    __syncthreads();  // every thread is done with the tile before the next copy lands
+  }
+}
+
+// Tensor map of g (int32, dims (n2, n1, n0), z innermost) with a
+// (32, 1, min(n0, 256)) box, built with the driver's cuTensorMapEncodeTiled
+// (resolved once through the runtime: no -lcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static int make_g_map(CUtensorMap *map, const int32_t *g, int64_t n0, int64_t n1, int64_t n2) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    VPB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    VPB_REQUIRE(p && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  const cuuint64_t dims[3] = {(cuuint64_t)n2, (cuuint64_t)n1, (cuuint64_t)n0};
+  const cuuint64_t strides[2] = {(cuuint64_t)n2 * 4, (cuuint64_t)n1 * n2 * 4};
+  const cuuint32_t box[3] = {32, 1, (cuuint32_t)(n0 < kTmaRows ? n0 : kTmaRows)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 3, const_cast<int32_t *>(g), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  VPB_REQUIRE(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return VPB_OK;
+}
+
+static size_t x_tile_rows(int64_t n0) {
+  const int64_t c = (n0 + kTmaRows - 1) / kTmaRows;
+  return (size_t)(c == 1 ? n0 : c * kTmaRows);
 }
 
 template <typename TIn, typename TOut>
@@ -936,32 +942,47 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], dou
   int32_t *g2 = reinterpret_cast<int32_t *>(reinterpret_cast<char *>(workspace) + align_up(vox * 2 > lrb ? vox * 2 : lrb, 256));
   const int64_t lines_z = n[0] * n[1];
   const int64_t maxd = n[0] > n[1] ? (n[0] > n[2] ? n[0] : n[2]) : (n[1] > n[2] ? n[1] : n[2]);
-  int rc;
+  int rc = VPB_OK;
   if (maxd <= 1024 && use_bits && n[0] <= 65535 && n[1] <= 65535 && n[2] % 4 == 0) {  // 16 B-aligned g rows
     VPB_REQUIRE(grid->occ_bits, "use_bits set but grid->occ_bits is null");
-    // Pass Z+Y fused from the occupancy words, then pass X.
+    // Pass Z+Y fused from the occupancy words, then pass X (TMA-staged).  The
+    // z chunks run in groups sized so one group's int32 g stays in L2 between
+    // the two launches (VPB_EDT_L2_MB, default 48 MB of the 126 MB L2).
     const size_t smem_zy = (size_t)n[1] * 32 * 4 + sizeof(SegLine) * 32;
-    const size_t smem_x = (size_t)n[0] * 32 * 4 + sizeof(SegLine) * 32;
+    const size_t smem_x = x_tile_rows(n[0]) * 32 * 4 + sizeof(SegLine) * 32 + 16;
     const bool wide = maxd > 512;
     auto kzy = wide ? edt_zy_kernel<true> : edt_zy_kernel<false>;
     auto kx = wide ? edt_x_kernel<true> : edt_x_kernel<false>;
-    if (smem_zy > 48 * 1024) VPB_CUDA(cudaFuncSetAttribute(kzy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
-    if (smem_x > 48 * 1024) VPB_CUDA(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
-    const unsigned zch = (unsigned)((n[2] + 31) / 32);
-    // per-line left/right source table (fits the u16 z-distance slot of the workspace)
-    uint32_t *lr = reinterpret_cast<uint32_t *>(workspace);
-    const int64_t lines = n[0] * n[1];
-    edt_line_lr_kernel<<<(unsigned)ceil_div(lines, 256), 256, 0, s>>>(
-        grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], (int)lo[2], (int)n[0], (int)n[1],
-        (int)n[2], lr);
-    rc = check_launch("edt_line_lr_kernel");
+    VPB_CUDA(cudaFuncSetAttribute(kzy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
+    VPB_CUDA(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
+    CUtensorMap gmap;
+    rc = make_g_map(&gmap, g2, n[0], n[1], n[2]);
     if (rc) return rc;
-    kzy<<<dim3(zch, (unsigned)n[0]), ETHREADS, smem_zy, s>>>(grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32),
-                                                             lo[0], lo[1], (int)lo[2], (int)n[1], (int)n[2], lr, g2);
-    rc = check_launch("edt_zy_kernel");
-    if (rc) return rc;
-    kx<<<dim3(zch, (unsigned)n[1]), ETHREADS, smem_x, s>>>(g2, (int)n[0], (int)n[1], (int)n[2], out_sq);
-    return check_launch("edt_x_kernel");
+    const int zch = (int)((n[2] + 31) / 32);
+    static const double l2_mb = getenv("VPB_EDT_L2_MB") ? atof(getenv("VPB_EDT_L2_MB")) : 80.0;
+    const double chunk_mb = (double)n[0] * (double)n[1] * 32.0 * 4.0 / 1048576.0;
+    int group = (int)(l2_mb / chunk_mb);
+    group = group < 1 ? 1 : (group > zch ? zch : group);
+    // persistent grids: every SM filled with as many CTAs as the smem allows
+    int occ_zy = 0, occ_x = 0;
+    VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_zy, kzy, ETHREADS, smem_zy));
+    VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, kx, ETHREADS, smem_x));
+    const int64_t slots_zy = (int64_t)sm_count() * (occ_zy > 0 ? occ_zy : 1);
+    const int64_t slots_x = (int64_t)sm_count() * (occ_x > 0 ? occ_x : 1);
+    for (int z0 = 0; z0 < zch; z0 += group) {
+      const int gz = z0 + group <= zch ? group : zch - z0;
+      const int64_t it_zy = (int64_t)gz * n[0], it_x = (int64_t)gz * n[1];
+      kzy<<<(unsigned)(it_zy < slots_zy ? it_zy : slots_zy), ETHREADS, smem_zy, s>>>(
+          grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], (int)lo[2], (int)n[0], (int)n[1],
+          (int)n[2], z0, gz, g2);
+      rc = check_launch("edt_zy_kernel");
+      if (rc) return rc;
+      kx<<<(unsigned)(it_x < slots_x ? it_x : slots_x), ETHREADS, smem_x, s>>>(gmap, (int)n[0], (int)n[1], (int)n[2],
+                                                                               z0, gz, out_sq);
+      rc = check_launch("edt_x_kernel");
+      if (rc) return rc;
+    }
+    return VPB_OK;
   }
   if (use_bits) {
     VPB_REQUIRE(grid->occ_bits, "use_bits set but grid->occ_bits is null");
