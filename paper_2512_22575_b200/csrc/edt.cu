@@ -405,11 +405,10 @@ static int launch_fh_smem(const TIn *in, TOut *out, int64_t n_outer, int64_t out
 // Every comparison is exact integer arithmetic, so the result equals the
 // reference's f64 FH (vp/mapping.py:458-483) bit for bit.
 // ---------------------------------------------------------------------------
-constexpr int KSEG = 4;
-constexpr int ETHREADS = 32 * KSEG;
-
+// KS segments per line (KS warps per CTA); SegLine<KS> holds the run bounds.
+template <int KS>
 struct SegLine {
-  int lo[KSEG], hi[KSEG];
+  int lo[KS], hi[KS];
 };
 
 struct Elem {
@@ -456,7 +455,8 @@ __device__ __forceinline__ bool dominated(const Elem &l, const Elem &p, const El
 }
 
 // previous / next non-empty element in segment order
-__device__ __forceinline__ bool prev_elem(const SegLine &S, int seg, int idx, int first_seg, int &ps, int &pi) {
+template <class SL>
+__device__ __forceinline__ bool prev_elem(const SL &S, int seg, int idx, int first_seg, int &ps, int &pi) {
   if (idx > S.lo[seg]) {
     ps = seg;
     pi = idx - 1;
@@ -471,7 +471,8 @@ __device__ __forceinline__ bool prev_elem(const SegLine &S, int seg, int idx, in
   return false;
 }
 
-__device__ __forceinline__ bool next_elem(const SegLine &S, int seg, int idx, int last_seg, int &ns, int &ni) {
+template <class SL>
+__device__ __forceinline__ bool next_elem(const SL &S, int seg, int idx, int last_seg, int &ns, int &ni) {
   if (idx + 1 < S.hi[seg]) {
     ns = seg;
     ni = idx + 1;
@@ -487,8 +488,8 @@ __device__ __forceinline__ bool next_elem(const SegLine &S, int seg, int idx, in
 }
 
 // Merge left run (segments a..b) with right run (b+1..c) of one line.
-template <bool WIDE>
-__device__ void merge_runs(uint32_t col, int B, SegLine &S, int a, int b, int c) {
+template <bool WIDE, class SL>
+__device__ void merge_runs(uint32_t col, int B, SL &S, int a, int b, int c) {
   int ls = -1, li = 0, rs = -1, ri = 0;
   for (int t = b; t >= a; --t)
     if (S.hi[t] > S.lo[t]) {
@@ -579,8 +580,8 @@ __device__ __forceinline__ void fwd_step(FwdState &S, uint32_t stk, int q, uint3
 // Merges of the 4 segment runs + output sweep (all ETHREADS threads; no early
 // return, so it can sit inside a persistent loop).  `k` = this thread's stack
 // top from the forward sweep.  dst_base[line + q * stride] receives output q.
-template <typename TOut, bool WIDE>
-__device__ __forceinline__ void fh_merge_output(uint32_t tile_s, SegLine *segs, int len, bool act, int k,
+template <typename TOut, bool WIDE, int KSEG>
+__device__ __forceinline__ void fh_merge_output(uint32_t tile_s, SegLine<KSEG> *segs, int len, bool act, int k,
                                                 TOut *__restrict__ dst_base, uint32_t stride) {
   const int tid = threadIdx.x;
   const int s = tid >> 5;     // segment = warp index
@@ -591,11 +592,12 @@ __device__ __forceinline__ void fh_merge_output(uint32_t tile_s, SegLine *segs, 
   segs[line].lo[s] = 0;
   segs[line].hi[s] = k + 1;
   __syncthreads();
-  // ---- merges: (0,1) and (2,3), then (01, 23) ----
-  if (act && (s == 0 || s == 2)) merge_runs<WIDE>(col, B, segs[line], s, s, s + 1);
-  __syncthreads();
-  if (act && s == 0) merge_runs<WIDE>(col, B, segs[line], 0, 1, 3);
-  __syncthreads();
+  // ---- pairwise merges up a binary tree: (0,1) (2,3) ..., then (01,23) ... ----
+#pragma unroll
+  for (int w = 1; w < KSEG; w <<= 1) {
+    if (act && (s & (2 * w - 1)) == 0) merge_runs<WIDE>(col, B, segs[line], s, s + w - 1, s + 2 * w - 1);
+    __syncthreads();
+  }
   if (act && q0 < q1) {
     // segment bounds of the merged envelope in registers (indexed only
     // through unrolled selects: no local memory)
@@ -608,9 +610,9 @@ __device__ __forceinline__ void fh_merge_output(uint32_t tile_s, SegLine *segs, 
     int total = 0;
 #pragma unroll
     for (int t = 0; t < KSEG; ++t) total += hi_[t] - lo_[t];
-    uint32_t off = (uint32_t)line + (uint32_t)q0 * stride;
+    TOut *dst = dst_base + line + (size_t)q0 * stride;
     if (total == 0) {
-      for (int q = q0; q < q1; ++q, off += stride) store_dist<TOut>(dst_base + off, -1);
+      for (int q = q0; q < q1; ++q, dst += stride) store_dist<TOut>(dst, -1);
     } else {
       auto rank_to = [&](int r, int &sg, int &ix) {
         sg = KSEG - 1;
@@ -672,7 +674,7 @@ __device__ __forceinline__ void fh_merge_output(uint32_t tile_s, SegLine *segs, 
       // Output sweep (vp/mapping.py:478-483): advance while the next
       // parabola's intersection lies strictly left of q; d(q) = (q - v)^2 + f.
       int f = cur.F - cur.v * cur.v;
-      for (int q = q0; q < q1; ++q, off += stride) {
+      for (int q = q0; q < q1; ++q, dst += stride) {
         while (left > 0 && boundary_lt<WIDE>(cur, nxt, q)) {
           cur = nxt;
           f = cur.F - cur.v * cur.v;
@@ -682,7 +684,7 @@ __device__ __forceinline__ void fh_merge_output(uint32_t tile_s, SegLine *segs, 
           }
         }
         const int d = q - cur.v;
-        store_dist<TOut>(dst_base + off, d * d + f);
+        store_dist<TOut>(dst, d * d + f);
       }
     }
   }
@@ -701,14 +703,14 @@ constexpr int kNoneHi = 0x20000;
 // and feeds it straight into the forward envelope sweep along y (no tile
 // fill pass).  Output: int32 g(x, y, z) = min over y' of (y - y')^2 + dz^2
 // (-1 = no source in the (x) plane).
-template <bool WIDE>
-__global__ void __launch_bounds__(ETHREADS) edt_zy_kernel(const uint32_t *__restrict__ bits, int64_t gy,
+template <bool WIDE, int KSEG>
+__global__ void __launch_bounds__(32 * KSEG) edt_zy_kernel(const uint32_t *__restrict__ bits, int64_t gy,
                                                           int64_t words_z, int64_t lo0, int64_t lo1, int lo2, int n0,
                                                           int n1, int n2, int zc_base, int gz,
                                                           int32_t *__restrict__ out) {
   extern __shared__ __align__(128) uint32_t smem[];
   const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(smem);    // [n1][32]
-  SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)n1 * 32);  // [32]
+  SegLine<KSEG> *segs = reinterpret_cast<SegLine<KSEG> *>(smem + (size_t)n1 * 32);  // [32]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nw = (n2 + 31) >> 5;
   const uint32_t le_mask = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
@@ -756,8 +758,12 @@ __global__ void __launch_bounds__(ETHREADS) edt_zy_kernel(const uint32_t *__rest
           }
         }
       }
-      const int rows = min(32, y1 - yb);
-      for (int t = 0; t < rows; ++t) {
+      // rows whose (x, y) line holds no source give +inf at every z: skip them
+      // (warp-uniform: the row data is shared by all 32 lanes)
+      uint32_t live = __ballot_sync(kFull, yr < y1 && (cw != 0u || L != kNoneLo || R != kNoneHi));
+      while (live) {
+        const int t = __ffs(live) - 1;
+        live &= live - 1u;
         const uint32_t word = __shfl_sync(kFull, cw, t);
         const int Lw = __shfl_sync(kFull, L, t), Rw = __shfl_sync(kFull, R, t);
         const uint32_t le = word & le_mask, ge = word & ge_mask;
@@ -767,7 +773,7 @@ __global__ void __launch_bounds__(ETHREADS) edt_zy_kernel(const uint32_t *__rest
         if (act) fwd_step<WIDE>(S, stk, yb + t, d < 0x8000 ? (uint32_t)(d * d) : kTileInf);
       }
     }
-    fh_merge_output<int32_t, WIDE>(tile_s, segs, n1, act, S.k, out + (x * n1) * (int64_t)n2 + zb, (uint32_t)n2);
+    fh_merge_output<int32_t, WIDE, KSEG>(tile_s, segs, n1, act, S.k, out + (x * n1) * (int64_t)n2 + zb, (uint32_t)n2);
     __syncthreads();  // the tile is reused by the next item
   }
 }
@@ -812,14 +818,14 @@ constexpr int kTmaRows = 256;  // TMA box rows per copy (the box-dimension limit
 // 128 B on one mbarrier; g holds -1 == kTileInf for "no source", so the copy
 // is raw; out-of-range z lanes arrive zero-filled and stay inactive), then the
 // segmented FH runs along x and writes the f32 field.
-template <bool WIDE>
-__global__ void __launch_bounds__(ETHREADS) edt_x_kernel(const __grid_constant__ CUtensorMap gmap, int n0, int n1,
+template <bool WIDE, int KSEG>
+__global__ void __launch_bounds__(32 * KSEG) edt_x_kernel(const __grid_constant__ CUtensorMap gmap, int n0, int n1,
                                                          int n2, int zc_base, int gz, float *__restrict__ out) {
   extern __shared__ __align__(128) uint32_t smem[];
   const int ncopies = (n0 + kTmaRows - 1) / kTmaRows;
   const int rows = ncopies == 1 ? n0 : ncopies * kTmaRows;
   uint32_t *tile = smem;                                                  // [rows][32]
-  SegLine *segs = reinterpret_cast<SegLine *>(smem + (size_t)rows * 32);  // [32]
+  SegLine<KSEG> *segs = reinterpret_cast<SegLine<KSEG> *>(smem + (size_t)rows * 32);  // [32]
   uint64_t *bar = reinterpret_cast<uint64_t *>(segs + 32);
   const uint32_t tile_s = (uint32_t)__cvta_generic_to_shared(tile);
   const int tid = threadIdx.x, lane = tid & 31, s = tid >> 5;
@@ -854,7 +860,7 @@ __global__ void __launch_bounds__(ETHREADS) edt_x_kernel(const __grid_constant__
         fwd_step<WIDE>(S, stk, q, e);
       }
     }
-    fh_merge_output<float, WIDE>(tile_s, segs, n0, act, S.k, out + (int64_t)y * n2 + zc * 32, (uint32_t)(n1 * n2));
+    fh_merge_output<float, WIDE, KSEG>(tile_s, segs, n0, act, S.k, out + (int64_t)y * n2 + zc * 32, (uint32_t)(n1 * n2));
     __syncthreads();  // every thread is done with the tile before the next copy lands
   }
 }
@@ -912,6 +918,49 @@ static int launch_fh(const TIn *in, TOut *out, int64_t n_outer, int64_t outer_st
   return check_launch("edt_pass_fh");
 }
 
+// The production path (lines <= 1024, z % 4 == 0): pass Z+Y fused from the
+// occupancy words, then pass X (TMA-staged), both persistent.  The z chunks
+// run in groups sized so one group's int32 g stays in L2 between the two
+// launches (VPB_EDT_L2_MB, default 80 MB of the 126 MB L2).
+template <bool WIDE, int KS>
+static int edt_tiled(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], int32_t *g2, float *out_sq,
+                     cudaStream_t s) {
+  const size_t smem_zy = (size_t)n[1] * 32 * 4 + sizeof(SegLine<KS>) * 32;
+  const size_t smem_x = x_tile_rows(n[0]) * 32 * 4 + sizeof(SegLine<KS>) * 32 + 16;
+  auto kzy = edt_zy_kernel<WIDE, KS>;
+  auto kx = edt_x_kernel<WIDE, KS>;
+  VPB_CUDA(cudaFuncSetAttribute(kzy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
+  VPB_CUDA(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
+  CUtensorMap gmap;
+  int rc = make_g_map(&gmap, g2, n[0], n[1], n[2]);
+  if (rc) return rc;
+  const int zch = (int)((n[2] + 31) / 32);
+  static const double l2_mb = getenv("VPB_EDT_L2_MB") ? atof(getenv("VPB_EDT_L2_MB")) : 80.0;
+  const double chunk_mb = (double)n[0] * (double)n[1] * 32.0 * 4.0 / 1048576.0;
+  int group = (int)(l2_mb / chunk_mb);
+  group = group < 1 ? 1 : (group > zch ? zch : group);
+  // persistent grids: every SM filled with as many CTAs as smem / registers allow
+  int occ_zy = 0, occ_x = 0;
+  VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_zy, kzy, 32 * KS, smem_zy));
+  VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, kx, 32 * KS, smem_x));
+  const int64_t slots_zy = (int64_t)sm_count() * (occ_zy > 0 ? occ_zy : 1);
+  const int64_t slots_x = (int64_t)sm_count() * (occ_x > 0 ? occ_x : 1);
+  for (int z0 = 0; z0 < zch; z0 += group) {
+    const int gz = z0 + group <= zch ? group : zch - z0;
+    const int64_t it_zy = (int64_t)gz * n[0], it_x = (int64_t)gz * n[1];
+    kzy<<<(unsigned)(it_zy < slots_zy ? it_zy : slots_zy), 32 * KS, smem_zy, s>>>(
+        grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], (int)lo[2], (int)n[0], (int)n[1],
+        (int)n[2], z0, gz, g2);
+    rc = check_launch("edt_zy_kernel");
+    if (rc) return rc;
+    kx<<<(unsigned)(it_x < slots_x ? it_x : slots_x), 32 * KS, smem_x, s>>>(gmap, (int)n[0], (int)n[1], (int)n[2], z0,
+                                                                             gz, out_sq);
+    rc = check_launch("edt_x_kernel");
+    if (rc) return rc;
+  }
+  return VPB_OK;
+}
+
 }  // namespace vpb
 
 using namespace vpb;
@@ -945,44 +994,14 @@ int vpb_edt3d(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], dou
   int rc = VPB_OK;
   if (maxd <= 1024 && use_bits && n[0] <= 65535 && n[1] <= 65535 && n[2] % 4 == 0) {  // 16 B-aligned g rows
     VPB_REQUIRE(grid->occ_bits, "use_bits set but grid->occ_bits is null");
-    // Pass Z+Y fused from the occupancy words, then pass X (TMA-staged).  The
-    // z chunks run in groups sized so one group's int32 g stays in L2 between
-    // the two launches (VPB_EDT_L2_MB, default 48 MB of the 126 MB L2).
-    const size_t smem_zy = (size_t)n[1] * 32 * 4 + sizeof(SegLine) * 32;
-    const size_t smem_x = x_tile_rows(n[0]) * 32 * 4 + sizeof(SegLine) * 32 + 16;
+    // 4 segments per line up to ~384 (6 CTAs x 4 warps per SM at 256), 8 for
+    // longer lines (the tile halves the CTAs per SM; 8 warps keep 24 resident)
+    static const int kseg_env = getenv("VPB_EDT_KSEG") ? atoi(getenv("VPB_EDT_KSEG")) : 0;
+    const int kseg = kseg_env ? kseg_env : ((n[0] > 384 || n[1] > 384) ? 8 : 4);
     const bool wide = maxd > 512;
-    auto kzy = wide ? edt_zy_kernel<true> : edt_zy_kernel<false>;
-    auto kx = wide ? edt_x_kernel<true> : edt_x_kernel<false>;
-    VPB_CUDA(cudaFuncSetAttribute(kzy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
-    VPB_CUDA(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
-    CUtensorMap gmap;
-    rc = make_g_map(&gmap, g2, n[0], n[1], n[2]);
-    if (rc) return rc;
-    const int zch = (int)((n[2] + 31) / 32);
-    static const double l2_mb = getenv("VPB_EDT_L2_MB") ? atof(getenv("VPB_EDT_L2_MB")) : 80.0;
-    const double chunk_mb = (double)n[0] * (double)n[1] * 32.0 * 4.0 / 1048576.0;
-    int group = (int)(l2_mb / chunk_mb);
-    group = group < 1 ? 1 : (group > zch ? zch : group);
-    // persistent grids: every SM filled with as many CTAs as the smem allows
-    int occ_zy = 0, occ_x = 0;
-    VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_zy, kzy, ETHREADS, smem_zy));
-    VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, kx, ETHREADS, smem_x));
-    const int64_t slots_zy = (int64_t)sm_count() * (occ_zy > 0 ? occ_zy : 1);
-    const int64_t slots_x = (int64_t)sm_count() * (occ_x > 0 ? occ_x : 1);
-    for (int z0 = 0; z0 < zch; z0 += group) {
-      const int gz = z0 + group <= zch ? group : zch - z0;
-      const int64_t it_zy = (int64_t)gz * n[0], it_x = (int64_t)gz * n[1];
-      kzy<<<(unsigned)(it_zy < slots_zy ? it_zy : slots_zy), ETHREADS, smem_zy, s>>>(
-          grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], (int)lo[2], (int)n[0], (int)n[1],
-          (int)n[2], z0, gz, g2);
-      rc = check_launch("edt_zy_kernel");
-      if (rc) return rc;
-      kx<<<(unsigned)(it_x < slots_x ? it_x : slots_x), ETHREADS, smem_x, s>>>(gmap, (int)n[0], (int)n[1], (int)n[2],
-                                                                               z0, gz, out_sq);
-      rc = check_launch("edt_x_kernel");
-      if (rc) return rc;
-    }
-    return VPB_OK;
+    if (kseg == 8)
+      return wide ? edt_tiled<true, 8>(grid, lo, n, g2, out_sq, s) : edt_tiled<false, 8>(grid, lo, n, g2, out_sq, s);
+    return wide ? edt_tiled<true, 4>(grid, lo, n, g2, out_sq, s) : edt_tiled<false, 4>(grid, lo, n, g2, out_sq, s);
   }
   if (use_bits) {
     VPB_REQUIRE(grid->occ_bits, "use_bits set but grid->occ_bits is null");
