@@ -544,6 +544,11 @@ template <>
 __device__ __forceinline__ void store_dist<float>(float *p, int v) {
   *p = v < 0 ? __int_as_float(0x7f800000) : (float)v;
 }
+// a finite value (>= 0)
+template <typename TOut>
+__device__ __forceinline__ void store_val(TOut *p, int v) {
+  *p = (TOut)v;
+}
 
 // Forward sweep of one thread's segment [q0, q1): lower envelope of the finite
 // parabolas, stack IN PLACE at column rows q0 + k (entry (F << 10) | v).
@@ -646,45 +651,57 @@ __device__ __forceinline__ void fh_merge_output(uint32_t tile_s, SegLine<KSEG> *
       rank_to(lo, cs, ci);
       int left = total - 1 - lo;  // parabolas after cur
       Elem cur = elem(cs, ci);
-      // next element: same segment, else the next non-empty one
-      auto step = [&](int &sg, int &ix) {
-        int h = hi_[0];
+      // the envelope in rank order: (ns, ni) walks the merged runs, with the
+      // current run's end cached in `hend`
+      auto sel = [&](const int(&a)[KSEG], int t) {
+        int v = a[0];
 #pragma unroll
-        for (int t = 1; t < KSEG; ++t) h = sg == t ? hi_[t] : h;
-        if (ix + 1 < h) {
-          ++ix;
-          return;
-        }
-        int ns = sg, ni = ix;
-#pragma unroll
-        for (int t = KSEG - 1; t >= 1; --t)
-          if (t > sg && hi_[t] > lo_[t]) {
-            ns = t;
-            ni = lo_[t];
-          }
-        sg = ns;
-        ix = ni;
+        for (int u = 1; u < KSEG; ++u) v = t == u ? a[u] : v;
+        return v;
       };
-      int ns = cs, ni = ci;
+      int ns = cs, ni = ci, hend = sel(hi_, cs);
+      auto advance = [&]() {
+        if (++ni >= hend) {
+          int t2 = ns;
+#pragma unroll
+          for (int t = KSEG - 1; t >= 1; --t)
+            if (t > ns && hi_[t] > lo_[t]) t2 = t;
+          ns = t2;
+          ni = sel(lo_, t2);
+          hend = sel(hi_, t2);
+        }
+      };
+      // advance to the next parabola at the first q with thr < q * den2
+      // (thr = F_n - F_c, den2 = 2 (v_n - v_c); |both| < 2^22, so 32-bit is
+      // exact for every line length on this path); none left: never.
+      int thr = 0x7fffffff, den2 = 0;
       Elem nxt = cur;
       if (left > 0) {
-        step(ns, ni);
+        advance();
         nxt = elem(ns, ni);
+        thr = nxt.F - cur.F;
+        den2 = 2 * (nxt.v - cur.v);
       }
       // Output sweep (vp/mapping.py:478-483): advance while the next
-      // parabola's intersection lies strictly left of q; d(q) = (q - v)^2 + f.
-      int f = cur.F - cur.v * cur.v;
+      // parabola's intersection lies strictly left of q; d(q) = (q - v)^2 + f
+      // (f >= 0: only finite parabolas are in the envelope).
+      int v = cur.v, f = cur.F - cur.v * cur.v;
       for (int q = q0; q < q1; ++q, dst += stride) {
-        while (left > 0 && boundary_lt<WIDE>(cur, nxt, q)) {
+        while (thr < q * den2) {
           cur = nxt;
-          f = cur.F - cur.v * cur.v;
+          v = cur.v;
+          f = cur.F - v * v;
+          thr = 0x7fffffff;
+          den2 = 0;
           if (--left > 0) {
-            step(ns, ni);
+            advance();
             nxt = elem(ns, ni);
+            thr = nxt.F - cur.F;
+            den2 = 2 * (nxt.v - v);
           }
         }
-        const int d = q - cur.v;
-        store_dist<TOut>(dst, d * d + f);
+        const int d = q - v;
+        store_val<TOut>(dst, d * d + f);
       }
     }
   }
