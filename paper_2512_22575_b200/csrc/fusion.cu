@@ -41,6 +41,10 @@ struct FusionArgs {
   const int *bbox;  // optional bounding rectangle of usable pixels (chunk early-out)
   float tauf;
   float bb_lo[3], bb_hi[3];
+  // frustum culling (fp32, conservative): camera centre and camera->world
+  // rotation, voxel-index box of the mask spheres (empty if none)
+  float camc[3], c2w[9];
+  int mask_i_lo[3], mask_i_hi[3];
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr2[VPB_MAX_MASK_SPHERES];
 };
@@ -102,152 +106,281 @@ __device__ __noinline__ bool exact_voxel(const FusionArgs &A, int64_t x, int64_t
   return true;
 }
 
-// One warp per (x, y) line of the box, looping over its z words.
-// grid: (ceil(n1 / 8), n0), 256 threads.
-__global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ FusionArgs A) {
-  const int lane = threadIdx.x & 31;
-  const int yi = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (yi >= A.n1) return;
-  const int64_t x = A.lo0 + blockIdx.y, y = A.lo1 + yi;
-  // ---- line constants of the conservative fp32 prefilter ----
-  // Decides, with explicit error bounds, the voxels whose reference result
-  // is certainly "skip" (behind the camera, outside the image, or landing on
-  // a pixel without a usable return).  Everything else -- robot-mask
-  // candidates, pixel-boundary ambiguities, voxels that fuse -- takes the
-  // exact fp64 path, so the result is bitwise the reference's.
-  const float axf = ((float)x + 0.5f) * A.voxf, ayf = ((float)y + 0.5f) * A.voxf;
-  const float pxf = A.of0 + axf, pyf = A.of1 + ayf;
-  const float qx0 = fmaf(A.rf[0], pxf, fmaf(A.rf[1], pyf, A.tf[0]));
-  const float qy0 = fmaf(A.rf[3], pxf, fmaf(A.rf[4], pyf, A.tf[1]));
-  const float qz0 = fmaf(A.rf[6], pxf, fmaf(A.rf[7], pyf, A.tf[2]));
-  // |q_f - q| <= dq: each centre coordinate is off by <= 2e-7 (|origin| +
-  // |(i + 1/2) voxel|), rotation entries are <= 1 and the three FMAs add
-  // <= 2e-7 of the row magnitude: 4e-7 in total, taken with a 2.5x margin.
-  const float dq = 1e-6f * (A.oabs + fabsf(axf) + fabsf(ayf) + A.azmax + A.tabs) + 1e-12f;
-  const bool line_mask = A.n_mask > 0 && pxf >= A.bb_lo[0] && pxf <= A.bb_hi[0] && pyf >= A.bb_lo[1] &&
-                         pyf <= A.bb_hi[1];
-  const int64_t gline = (x * A.gy + y) * A.gz;
-  int bb_u0 = 0, bb_u1 = -1, bb_v0 = 0, bb_v1 = -1;
+// The voxels the reference can touch in one update are (a) those inside the
+// pyramid from the camera centre through the rectangle of usable pixels, out
+// to the farthest usable return + tau, and (b) those inside a mask sphere.
+// Per CTA: the voxel-index box of (a) from the apex and the 4 far corners,
+// and of (b) from the mask AABB.  Per (x, y) line of that footprint: the
+// z-interval of (a), solved analytically from the 6 linear constraints
+// (in front of / before the far plane / inside the 4 side planes, each
+// a + b z >= 0 in camera space), widened by 2 pixels and 2 voxels, united
+// with the mask interval.  Only those voxels run the per-voxel prefilter
+// below, which makes the exact decision (the culling is conservative: it may
+// include voxels the reference skips, never the reverse).
+struct Interval {
+  int lo, hi;  // inclusive, empty if lo > hi
+};
+
+__device__ __forceinline__ void clip_lin(float a, float b, float &zlo, float &zhi) {
+  // keep z with a + b z >= 0
+  if (b > 0.0f) zlo = fmaxf(zlo, -a / b);
+  else if (b < 0.0f) zhi = fminf(zhi, -a / b);
+  else if (a < 0.0f) zhi = -1e30f;
+}
+
+struct Frustum {
+  int ok;                // usable pixels exist
+  float ulo, uhi, vlo, vhi, dfar;
+  int xlo, xhi, ylo, yhi;  // footprint lines (box-clipped voxel indices)
+};
+
+__device__ void frustum_setup(const FusionArgs &A, Frustum &F) {
+  int u0 = 0, u1 = -1, v0 = 0, v1 = -1;
+  float dmax = 0.0f;
   if (A.bbox) {
-    bb_u0 = __ldg(A.bbox + 0);
-    bb_u1 = __ldg(A.bbox + 1);
-    bb_v0 = __ldg(A.bbox + 2);
-    bb_v1 = __ldg(A.bbox + 3);
+    u0 = __ldcg(A.bbox + 0);
+    u1 = __ldcg(A.bbox + 1);
+    v0 = __ldcg(A.bbox + 2);
+    v1 = __ldcg(A.bbox + 3);
+    dmax = __int_as_float(__ldcg(A.bbox + 4));
   }
-  // ---- range early-out (warp-uniform): the voxel centres of z in [za, zb]
-  // lie on a segment whose image is the segment between its endpoints'
-  // projections (qz > 0 at both ends => along it).  If that pixel range,
-  // widened by the error bound, misses every usable pixel, every voxel of the
-  // range is a reference "skip" -- unless the range may touch a mask sphere.
-  auto range_skip = [&](int64_t za, int64_t zb) -> bool {
-    const float pza = A.of2 + ((float)za + 0.5f) * A.voxf, pzb = A.of2 + ((float)zb + 0.5f) * A.voxf;
-    const bool maybe_mask = line_mask && !(pzb < A.bb_lo[2] || pza > A.bb_hi[2]);
-    if (maybe_mask) return false;
-    const float qza = fmaf(A.rf[8], pza, qz0), qzb = fmaf(A.rf[8], pzb, qz0);
-    if (qza < -dq && qzb < -dq) return true;  // whole range behind the camera
-    if (!(qza > 2.0f * dq && qzb > 2.0f * dq)) return false;
-    const float ia = __fdividef(1.0f, qza), ib = __fdividef(1.0f, qzb);
-    const float qxa = fmaf(A.rf[2], pza, qx0), qxb = fmaf(A.rf[2], pzb, qx0);
-    const float qya = fmaf(A.rf[5], pza, qy0), qyb = fmaf(A.rf[5], pzb, qy0);
-    const float ua = fmaf(A.fxf * qxa, ia, A.cxh), ub = fmaf(A.fxf * qxb, ib, A.cxh);
-    const float va = fmaf(A.fyf * qya, ia, A.cyh), vb = fmaf(A.fyf * qyb, ib, A.cyh);
-    const float ima = fmaxf(ia, ib);
-    const float du = A.ku * dq * (fmaxf(fabsf(qxa), fabsf(qxb)) + fmaxf(qza, qzb) + dq) * ima * ima +
-                     1e-6f * fmaxf(fabsf(ua), fabsf(ub)) + A.au;
-    const float dv = A.kv * dq * (fmaxf(fabsf(qya), fabsf(qyb)) + fmaxf(qza, qzb) + dq) * ima * ima +
-                     1e-6f * fmaxf(fabsf(va), fabsf(vb)) + A.av;
-    const float u_lo = fminf(ua, ub) - du - 1.0f, u_hi = fmaxf(ua, ub) + du + 1.0f;
-    const float v_lo = fminf(va, vb) - dv - 1.0f, v_hi = fmaxf(va, vb) + dv + 1.0f;
-    return bb_u1 < bb_u0 || u_hi < (float)bb_u0 || u_lo > (float)(bb_u1 + 1) || v_hi < (float)bb_v0 ||
-           v_lo > (float)(bb_v1 + 1);
-  };
-  // whole line first: most lines of a large box never meet a usable pixel
-  if (A.bbox && range_skip(A.lo2, A.lo2 + A.n2 - 1)) return;
-  for (int64_t wz = A.wz_begin; wz < A.wz_begin + A.wz_count; ++wz) {
-    const int64_t z = wz * 32 + lane;
-    const bool in_box = (z >= A.lo2) && (z < A.lo2 + A.n2);
-    if (A.bbox) {
-      const int64_t za = wz * 32 > A.lo2 ? wz * 32 : A.lo2;
-      const int64_t zb = (wz * 32 + 31) < (A.lo2 + A.n2 - 1) ? (wz * 32 + 31) : (A.lo2 + A.n2 - 1);
-      if (range_skip(za, zb)) continue;
+  float lo[3] = {1e30f, 1e30f, 1e30f}, hi[3] = {-1e30f, -1e30f, -1e30f};
+  F.ok = A.bbox == nullptr || u1 >= u0;
+  if (F.ok) {
+    // pixel index floor(u + 1/2) in [u0, u1] <=> u in [u0 - 1/2, u1 + 1/2);
+    // 2 pixels and 2 voxels of margin
+    F.ulo = (float)u0 - 2.5f;
+    F.uhi = (float)u1 + 2.5f;
+    F.vlo = (float)v0 - 2.5f;
+    F.vhi = (float)v1 + 2.5f;
+    F.dfar = A.bbox ? dmax + A.tauf + 2.0f * A.voxf : 3.0e30f;
+    if (!A.bbox) {  // no rectangle (vpb_fuse_voxels): the whole image, any depth
+      F.ulo = -2.5f;
+      F.uhi = (float)A.width + 1.5f;
+      F.vlo = -2.5f;
+      F.vhi = (float)A.height + 1.5f;
     }
-    bool exact = false;
-    int fast = 0;  // 1 = certain hit, 2 = certain miss (fp32 classification)
-    if (in_box) {
-      const float pzf = A.of2 + ((float)z + 0.5f) * A.voxf;
-      if (line_mask && pzf >= A.bb_lo[2] && pzf <= A.bb_hi[2]) {
-        exact = true;  // possibly inside a mask sphere
-      } else {
-        const float qzf = fmaf(A.rf[8], pzf, qz0);
-        if (qzf < -dq) {
-          // qz <= 0 for sure: the reference skips this voxel
-        } else if (qzf <= 2.0f * dq + 1e-30f) {
-          exact = true;
+    if (A.bbox) {
+      for (int k = 0; k < 3; ++k) lo[k] = hi[k] = A.camc[k];
+      for (int c = 0; c < 4; ++c) {
+        const float u = c & 1 ? F.uhi : F.ulo, v = c & 2 ? F.vhi : F.vlo;
+        const float dc[3] = {(u - (float)A.cx) / A.fxf * F.dfar, (v - (float)A.cy) / A.fyf * F.dfar, F.dfar};
+        for (int k = 0; k < 3; ++k) {
+          const float w = A.camc[k] + A.c2w[3 * k + 0] * dc[0] + A.c2w[3 * k + 1] * dc[1] + A.c2w[3 * k + 2] * dc[2];
+          lo[k] = fminf(lo[k], w);
+          hi[k] = fmaxf(hi[k], w);
+        }
+      }
+    } else {
+      for (int k = 0; k < 3; ++k) {
+        lo[k] = -3.0e30f;
+        hi[k] = 3.0e30f;
+      }
+    }
+  }
+  // voxel-index footprint: frustum box U mask box, clipped to the update box
+  int ilo[2], ihi[2];
+  const float org[2] = {A.of0, A.of1};
+  const int64_t blo[2] = {A.lo0, A.lo1}, bn[2] = {A.n0, A.n1};
+  for (int k = 0; k < 2; ++k) {
+    int a = INT_MAX, b = INT_MIN;
+    if (F.ok) {
+      const float fa = fmaxf(fminf((lo[k] - org[k]) / A.voxf - 0.5f, 2.0e9f), -2.0e9f);
+      const float fb = fmaxf(fminf((hi[k] - org[k]) / A.voxf - 0.5f, 2.0e9f), -2.0e9f);
+      a = (int)floorf(fa) - 2;
+      b = (int)ceilf(fb) + 2;
+    }
+    if (A.n_mask > 0) {
+      a = min(a, A.mask_i_lo[k]);
+      b = max(b, A.mask_i_hi[k]);
+    }
+    ilo[k] = max(a, (int)blo[k]);
+    ihi[k] = min(b, (int)(blo[k] + bn[k] - 1));
+  }
+  F.xlo = ilo[0], F.xhi = ihi[0], F.ylo = ilo[1], F.yhi = ihi[1];
+}
+
+// z-interval (voxel indices, box-clipped) of line (x, y) that may be touched
+__device__ __forceinline__ void line_intervals(const FusionArgs &A, const Frustum &F, int64_t x, int64_t y,
+                                               Interval &a, Interval &m) {
+  const int zb0 = (int)A.lo2, zb1 = (int)(A.lo2 + A.n2 - 1);
+  a.lo = 1, a.hi = 0;
+  m.lo = 1, m.hi = 0;
+  const float px = A.of0 + ((float)x + 0.5f) * A.voxf, py = A.of1 + ((float)y + 0.5f) * A.voxf;
+  if (F.ok) {
+    // camera coordinates along the line: q(z) = qa + z qb
+    const float pz0 = A.of2 + 0.5f * A.voxf;
+    float qa[3], qb[3];
+    for (int k = 0; k < 3; ++k) {
+      qa[k] = A.rf[3 * k + 0] * px + A.rf[3 * k + 1] * py + A.rf[3 * k + 2] * pz0 + A.tf[k];
+      qb[k] = A.rf[3 * k + 2] * A.voxf;
+    }
+    float zlo = (float)zb0 - 2.0f, zhi = (float)zb1 + 2.0f;
+    const float eps = 2e-3f;  // depth slab around the camera plane kept whole (see below)
+    clip_lin(qa[2] + eps, qb[2], zlo, zhi);        // qz >= -eps
+    clip_lin(F.dfar - qa[2], -qb[2], zlo, zhi);    // qz <= dfar
+    float flo = zlo, fhi = zhi;
+    const float fx = A.fxf, fy = A.fyf, cx = (float)A.cx, cy = (float)A.cy;
+    // u >= ulo: fx qx - (ulo - cx) qz >= 0 ; u <= uhi: (uhi - cx) qz - fx qx >= 0 (for qz > 0)
+    clip_lin(fx * qa[0] - (F.ulo - cx) * qa[2], fx * qb[0] - (F.ulo - cx) * qb[2], flo, fhi);
+    clip_lin((F.uhi - cx) * qa[2] - fx * qa[0], (F.uhi - cx) * qb[2] - fx * qb[0], flo, fhi);
+    clip_lin(fy * qa[1] - (F.vlo - cy) * qa[2], fy * qb[1] - (F.vlo - cy) * qb[2], flo, fhi);
+    clip_lin((F.vhi - cy) * qa[2] - fy * qa[1], (F.vhi - cy) * qb[2] - fy * qb[1], flo, fhi);
+    if (flo <= fhi) {
+      a.lo = max(zb0, (int)floorf(flo) - 2);
+      a.hi = min(zb1, (int)ceilf(fhi) + 2);
+    }
+    // Within eps of the camera plane the side-plane test loses its margin to
+    // fp32 rounding: if the line passes within 2 voxels of the camera centre,
+    // the voxels there with -eps <= qz <= eps are kept as well.
+    const float dx = px - A.camc[0], dy = py - A.camc[1];
+    if (dx * dx + dy * dy <= 4.0f * A.voxf * A.voxf + 1e-6f && qb[2] != 0.0f) {
+      float nlo = (float)zb0, nhi = (float)zb1;
+      clip_lin(qa[2] + eps, qb[2], nlo, nhi);
+      clip_lin(eps - qa[2], -qb[2], nlo, nhi);
+      if (nlo <= nhi) {
+        const int l = max(zb0, (int)floorf(nlo) - 2), h = min(zb1, (int)ceilf(nhi) + 2);
+        if (a.lo > a.hi) {
+          a.lo = l;
+          a.hi = h;
         } else {
-          const float qxf = fmaf(A.rf[2], pzf, qx0);
-          const float qyf = fmaf(A.rf[5], pzf, qy0);
-          const float iz = __fdividef(1.0f, qzf);  // <= 2 ulp, inside the margins below
-          const float ue = fmaf(A.fxf * qxf, iz, A.cxh);  // u + 1/2
-          const float ve = fmaf(A.fyf * qyf, iz, A.cyh);
-          // |d u / d q| <= fx (|qx| + qz) / (qz (qz - dq)) <= 8 fx (|qx_f| + qz_f + dq) / qz_f^2
-          // for qz_f > 2 dq; 10 fx taken.  Relative fp32 error of the
-          // projection itself <= 4 ulp: 1e-6 |u| + 1e-6 |c| + 4e-5.
-          const float iz2 = iz * iz;
-          const float du = A.ku * dq * (fabsf(qxf) + qzf + dq) * iz2 + 1e-6f * fabsf(ue) + A.au;
-          const float dv = A.kv * dq * (fabsf(qyf) + qzf + dq) * iz2 + 1e-6f * fabsf(ve) + A.av;
-          if (!(ue < -du || ue >= A.wf + du || ve < -dv || ve >= A.hf + dv)) {
-            const float fu = floorf(ue), fv = floorf(ve);
-            if ((ue - fu <= du) || (fu + 1.0f - ue <= du) || (ve - fv <= dv) || (fv + 1.0f - ve <= dv) ||
-                fu < 0.0f || fu >= A.wf || fv < 0.0f || fv >= A.hf) {
-              exact = true;  // pixel index not certain
-            } else {
-              const int pix = (int)fv * (int)A.width + (int)fu;
-              bool usable;
-              if (A.usable) {
-                usable = __ldg(A.pixel_masked + pix) == 2;
-              } else {
-                const double m = __ldg(A.depth + pix);
-                usable = (__ldg(A.pixel_masked + pix) & 1) == 0 && m >= A.d_min && m <= A.d_max;
-              }
-              if (usable) {
-                // classification |qz - D| <= tau (hit) / qz < D - tau (miss) /
-                // occluded, decided in fp32 when clear of both boundaries
-                const float mf = (float)__ldg(A.depth + pix);
-                const float dd = qzf - mf;
-                const float e = dq + 2e-7f * (fabsf(mf) + A.tauf) + 1e-6f;
-                if (fabsf(dd) <= A.tauf - e) fast = 1;
-                else if (dd < -A.tauf - e) fast = 2;
-                else if (!(dd > A.tauf + e)) exact = true;  // near a class boundary
-                // else: certainly occluded -> skip
-              }
-            }
-          }
-          // else: certainly outside the image -> skip
+          a.lo = min(a.lo, l);
+          a.hi = max(a.hi, h);
         }
       }
     }
-    bool touched = false;
-    double newval = 0.0;
-    if (fast) {
-      // certain hit / miss: the reference's fp64 update, bit for bit
-      const int64_t g = gline + z;
-      double value = dadd(A.log_odds[g], fast == 1 ? A.l_hit : A.l_miss);
-      if (value < A.l_min) value = A.l_min;
-      else if (value > A.l_max) value = A.l_max;
-      A.log_odds[g] = value;
-      A.observed[g] = 1;
-      newval = value;
-      touched = true;
-    } else if (exact) {
-      touched = exact_voxel(A, x, y, z, gline + z, &newval);
-    }
-    if (A.occ_bits != nullptr) {
-      const unsigned touched_mask = __ballot_sync(kFull, touched);
-      if (touched_mask != 0u) {
-        const unsigned occ_mask = __ballot_sync(kFull, touched && newval >= A.l_thr);
-        if (lane == 0) {
-          uint32_t *w = A.occ_bits + (x * A.gy + y) * A.words_z + wz;
-          *w = (*w & ~touched_mask) | (occ_mask & touched_mask);
+  }
+  if (A.n_mask > 0 && x >= A.mask_i_lo[0] && x <= A.mask_i_hi[0] && y >= A.mask_i_lo[1] && y <= A.mask_i_hi[1]) {
+    m.lo = max(zb0, A.mask_i_lo[2]);
+    m.hi = min(zb1, A.mask_i_hi[2]);
+  }
+}
+
+// Persistent: each warp takes (x, y) lines of the footprint; per line the
+// 32-voxel words overlapping its intervals run the per-voxel prefilter.
+__global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ FusionArgs A) {
+  __shared__ Frustum Fs;
+  if (threadIdx.x == 0) frustum_setup(A, Fs);
+  __syncthreads();
+  const Frustum F = Fs;
+  const int lane = threadIdx.x & 31;
+  const int nx = F.xhi - F.xlo + 1, ny = F.yhi - F.ylo + 1;
+  if (nx <= 0 || ny <= 0) return;
+  const int64_t lines = (int64_t)nx * ny;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t li = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); li < lines; li += warps) {
+    const int64_t x = F.xlo + li / ny, y = F.ylo + li % ny;
+    Interval ia, im;
+    line_intervals(A, F, x, y, ia, im);
+    if (ia.lo > ia.hi && im.lo > im.hi) continue;
+    // ---- line constants of the conservative fp32 prefilter ----
+    // Decides, with explicit error bounds, the voxels whose reference result
+    // is certainly "skip" (behind the camera, outside the image, or landing
+    // on a pixel without a usable return).  Everything else -- robot-mask
+    // candidates, pixel-boundary ambiguities, voxels that fuse -- takes the
+    // exact fp64 path, so the result is bitwise the reference's.
+    const float axf = ((float)x + 0.5f) * A.voxf, ayf = ((float)y + 0.5f) * A.voxf;
+    const float pxf = A.of0 + axf, pyf = A.of1 + ayf;
+    const float qx0 = fmaf(A.rf[0], pxf, fmaf(A.rf[1], pyf, A.tf[0]));
+    const float qy0 = fmaf(A.rf[3], pxf, fmaf(A.rf[4], pyf, A.tf[1]));
+    const float qz0 = fmaf(A.rf[6], pxf, fmaf(A.rf[7], pyf, A.tf[2]));
+    // |q_f - q| <= dq: each centre coordinate is off by <= 2e-7 (|origin| +
+    // |(i + 1/2) voxel|), rotation entries are <= 1 and the three FMAs add
+    // <= 2e-7 of the row magnitude: 4e-7 in total, taken with a 2.5x margin.
+    const float dq = 1e-6f * (A.oabs + fabsf(axf) + fabsf(ayf) + A.azmax + A.tabs) + 1e-12f;
+    const bool line_mask = A.n_mask > 0 && pxf >= A.bb_lo[0] && pxf <= A.bb_hi[0] && pyf >= A.bb_lo[1] &&
+                           pyf <= A.bb_hi[1];
+    const int64_t gline = (x * A.gy + y) * A.gz;
+    // words overlapping the union of the two intervals (hull when they overlap)
+    const int zlo = ia.lo <= ia.hi ? (im.lo <= im.hi ? min(ia.lo, im.lo) : ia.lo) : im.lo;
+    const int zhi = ia.lo <= ia.hi ? (im.lo <= im.hi ? max(ia.hi, im.hi) : ia.hi) : im.hi;
+    const bool gap = ia.lo <= ia.hi && im.lo <= im.hi && (ia.hi < im.lo - 32 || im.hi < ia.lo - 32);
+    for (int64_t wz = zlo >> 5; wz <= (zhi >> 5); ++wz) {
+      if (gap) {  // two separate intervals: skip the words between them
+        const int w0 = (int)wz * 32, w1 = w0 + 31;
+        const bool in_a = !(w1 < ia.lo || w0 > ia.hi), in_m = !(w1 < im.lo || w0 > im.hi);
+        if (!in_a && !in_m) continue;
+      }
+      const int64_t z = wz * 32 + lane;
+      const bool in_box = (z >= A.lo2) && (z < A.lo2 + A.n2);
+      bool exact = false;
+      int fast = 0;  // 1 = certain hit, 2 = certain miss (fp32 classification)
+      if (in_box) {
+        const float pzf = A.of2 + ((float)z + 0.5f) * A.voxf;
+        if (line_mask && pzf >= A.bb_lo[2] && pzf <= A.bb_hi[2]) {
+          exact = true;  // possibly inside a mask sphere
+        } else {
+          const float qzf = fmaf(A.rf[8], pzf, qz0);
+          if (qzf < -dq) {
+            // qz <= 0 for sure: the reference skips this voxel
+          } else if (qzf <= 2.0f * dq + 1e-30f) {
+            exact = true;
+          } else {
+            const float qxf = fmaf(A.rf[2], pzf, qx0);
+            const float qyf = fmaf(A.rf[5], pzf, qy0);
+            const float iz = __fdividef(1.0f, qzf);  // <= 2 ulp, inside the margins below
+            const float ue = fmaf(A.fxf * qxf, iz, A.cxh);  // u + 1/2
+            const float ve = fmaf(A.fyf * qyf, iz, A.cyh);
+            // |d u / d q| <= fx (|qx| + qz) / (qz (qz - dq)) <= 8 fx (|qx_f| + qz_f + dq) / qz_f^2
+            // for qz_f > 2 dq; 10 fx taken.  Relative fp32 error of the
+            // projection itself <= 4 ulp: 1e-6 |u| + 1e-6 |c| + 4e-5.
+            const float iz2 = iz * iz;
+            const float du = A.ku * dq * (fabsf(qxf) + qzf + dq) * iz2 + 1e-6f * fabsf(ue) + A.au;
+            const float dv = A.kv * dq * (fabsf(qyf) + qzf + dq) * iz2 + 1e-6f * fabsf(ve) + A.av;
+            if (!(ue < -du || ue >= A.wf + du || ve < -dv || ve >= A.hf + dv)) {
+              const float fu = floorf(ue), fv = floorf(ve);
+              if ((ue - fu <= du) || (fu + 1.0f - ue <= du) || (ve - fv <= dv) || (fv + 1.0f - ve <= dv) ||
+                  fu < 0.0f || fu >= A.wf || fv < 0.0f || fv >= A.hf) {
+                exact = true;  // pixel index not certain
+              } else {
+                const int pix = (int)fv * (int)A.width + (int)fu;
+                bool usable;
+                if (A.usable) {
+                  usable = __ldg(A.pixel_masked + pix) == 2;
+                } else {
+                  const double m = __ldg(A.depth + pix);
+                  usable = (__ldg(A.pixel_masked + pix) & 1) == 0 && m >= A.d_min && m <= A.d_max;
+                }
+                if (usable) {
+                  // classification |qz - D| <= tau (hit) / qz < D - tau (miss) /
+                  // occluded, decided in fp32 when clear of both boundaries
+                  const float mf = (float)__ldg(A.depth + pix);
+                  const float dd = qzf - mf;
+                  const float e = dq + 2e-7f * (fabsf(mf) + A.tauf) + 1e-6f;
+                  if (fabsf(dd) <= A.tauf - e) fast = 1;
+                  else if (dd < -A.tauf - e) fast = 2;
+                  else if (!(dd > A.tauf + e)) exact = true;  // near a class boundary
+                  // else: certainly occluded -> skip
+                }
+              }
+            }
+            // else: certainly outside the image -> skip
+          }
+        }
+      }
+      bool touched = false;
+      double newval = 0.0;
+      if (fast) {
+        // certain hit / miss: the reference's fp64 update, bit for bit
+        const int64_t g = gline + z;
+        double value = dadd(A.log_odds[g], fast == 1 ? A.l_hit : A.l_miss);
+        if (value < A.l_min) value = A.l_min;
+        else if (value > A.l_max) value = A.l_max;
+        A.log_odds[g] = value;
+        A.observed[g] = 1;
+        newval = value;
+        touched = true;
+      } else if (exact) {
+        touched = exact_voxel(A, x, y, z, gline + z, &newval);
+      }
+      if (A.occ_bits != nullptr) {
+        const unsigned touched_mask = __ballot_sync(kFull, touched);
+        if (touched_mask != 0u) {
+          const unsigned occ_mask = __ballot_sync(kFull, touched && newval >= A.l_thr);
+          if (lane == 0) {
+            uint32_t *w = A.occ_bits + (x * A.gy + y) * A.words_z + wz;
+            *w = (*w & ~touched_mask) | (occ_mask & touched_mask);
+          }
         }
       }
     }
@@ -301,19 +434,23 @@ __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constan
     // rectangle of the usable pixels: CTA reduction, then the last CTA
     // (ticket) reduces the CTA rectangles -- no atomics on the rectangle and
     // no memset before the launch
-    __shared__ int red[4][8];
+    // plus the farthest usable return (float bits rounded up: positive
+    // floats order like their bit patterns)
+    __shared__ int red[5][8];
     __shared__ unsigned last;
     const bool use = code == 2;
     int r0 = __reduce_min_sync(kFull, use ? (int)uu : INT_MAX);
     int r1 = __reduce_max_sync(kFull, use ? (int)uu : INT_MIN);
     int r2 = __reduce_min_sync(kFull, use ? (int)vv : INT_MAX);
     int r3 = __reduce_max_sync(kFull, use ? (int)vv : INT_MIN);
+    int r4 = __reduce_max_sync(kFull, use ? __float_as_int(__double2float_ru(d)) : 0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
       red[0][warp] = r0;
       red[1][warp] = r1;
       red[2][warp] = r2;
       red[3][warp] = r3;
+      red[4][warp] = r4;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -322,29 +459,32 @@ __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constan
         r1 = max(r1, red[1][w]);
         r2 = min(r2, red[2][w]);
         r3 = max(r3, red[3][w]);
+        r4 = max(r4, red[4][w]);
       }
-      int *pp = A.partials + 4 * blockIdx.x;
-      pp[0] = r0, pp[1] = r1, pp[2] = r2, pp[3] = r3;
+      int *pp = A.partials + 8 * blockIdx.x;
+      pp[0] = r0, pp[1] = r1, pp[2] = r2, pp[3] = r3, pp[4] = r4;
       __threadfence();
       last = atomicAdd(A.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
     }
     __syncthreads();
     if (last && threadIdx.x < 32) {
       __threadfence();
-      int m0 = INT_MAX, m1 = INT_MIN, m2 = INT_MAX, m3 = INT_MIN;
+      int m0 = INT_MAX, m1 = INT_MIN, m2 = INT_MAX, m3 = INT_MIN, m4 = 0;
       for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
-        const int *pp = A.partials + 4 * b;
+        const int *pp = A.partials + 8 * b;
         m0 = min(m0, __ldcg(pp + 0));
         m1 = max(m1, __ldcg(pp + 1));
         m2 = min(m2, __ldcg(pp + 2));
         m3 = max(m3, __ldcg(pp + 3));
+        m4 = max(m4, __ldcg(pp + 4));
       }
       m0 = __reduce_min_sync(kFull, m0);
       m1 = __reduce_max_sync(kFull, m1);
       m2 = __reduce_min_sync(kFull, m2);
       m3 = __reduce_max_sync(kFull, m3);
+      m4 = __reduce_max_sync(kFull, m4);
       if (threadIdx.x == 0) {
-        A.bbox[0] = m0, A.bbox[1] = m1, A.bbox[2] = m2, A.bbox[3] = m3;
+        A.bbox[0] = m0, A.bbox[1] = m1, A.bbox[2] = m2, A.bbox[3] = m3, A.bbox[4] = m4;
         *A.counter = 0u;
       }
     }
@@ -425,8 +565,8 @@ static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const 
   A.n_mask = (int)n_mask;
   A.encode_usable = encode;
   A.bbox = bbox;
-  if (bbox) {  // scratch after the rectangle: [ticket, pad..., CTA rectangles]
-    A.counter = reinterpret_cast<unsigned *>(bbox + 4);
+  if (bbox) {  // [u0 u1 v0 v1 dmax_bits - ticket -] then 8 ints per CTA
+    A.counter = reinterpret_cast<unsigned *>(bbox + 6);
     A.partials = bbox + 8;
   }
   A.pad = pad;
@@ -502,9 +642,23 @@ static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
   A.hf = (float)A.height;
   // the fp32 prefilter assumes an orthonormal world->camera rotation and a
   // scene within float range; anything else simply takes the exact path
-  VPB_REQUIRE(A.n0 <= 65535, "box too large for the fusion grid");
-  dim3 launch_grid((unsigned)ceil_div(A.n1, 8), (unsigned)A.n0);
-  fuse_kernel<<<launch_grid, 256, 0, as_stream(stream)>>>(A);
+  for (int k = 0; k < 3; ++k) A.camc[k] = (float)cam->pose_t[k];
+  for (int k = 0; k < 9; ++k) A.c2w[k] = (float)cam->pose_r[k];
+  for (int k = 0; k < 3; ++k) {
+    // voxel indices whose fp32 centre can fall in the padded mask box (+1)
+    const double o = k == 0 ? A.origin0 : (k == 1 ? A.origin1 : A.origin2);
+    if (n_mask > 0) {
+      A.mask_i_lo[k] = (int)fmax(-2.0e9, floor(((double)A.bb_lo[k] - o) / A.voxel - 0.5) - 1.0);
+      A.mask_i_hi[k] = (int)fmin(2.0e9, ceil(((double)A.bb_hi[k] - o) / A.voxel - 0.5) + 1.0);
+    } else {
+      A.mask_i_lo[k] = 1;
+      A.mask_i_hi[k] = 0;
+    }
+  }
+  // persistent: warps stride over the footprint lines each CTA derives
+  const int64_t max_ctas = ceil_div(A.n0 * A.n1, 8);
+  const int64_t ctas = max_ctas < (int64_t)sm_count() * 8 ? max_ctas : (int64_t)sm_count() * 8;
+  fuse_kernel<<<(unsigned)ctas, 256, 0, as_stream(stream)>>>(A);
   return check_launch("fuse_kernel");
 }
 
@@ -521,7 +675,7 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3
 
 int64_t vpb_pixel_scratch_bytes(int64_t width, int64_t height) {
   const int64_t npx = width * height;
-  return (int64_t)align_up((size_t)npx, 16) + 32 + 16 * ceil_div(npx > 0 ? npx : 1, 256) + 64;
+  return (int64_t)align_up((size_t)npx, 16) + 32 + 32 * ceil_div(npx > 0 ? npx : 1, 256) + 64;
 }
 
 int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,

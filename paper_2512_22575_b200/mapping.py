@@ -66,6 +66,14 @@ class VoxelBox:
     def slices(self):
         return tuple(slice(l, h) for l, h in zip(self.lo, self.hi))
 
+    def native(self):
+        """(lo, shape) as cached int64[3] ctypes arrays."""
+        n = self.__dict__.get("_native")
+        if n is None:
+            n = (i64x3(self.lo), i64x3(self.shape))
+            object.__setattr__(self, "_native", n)
+        return n
+
 
 class VoxelGrid:
     """Dense occupancy grid in device memory (vp/mapping.py:76-140).
@@ -94,6 +102,8 @@ class VoxelGrid:
         self._occ_bits = torch.zeros(words, dtype=torch.int32, device=self.device)
         self._bits_valid = True
         self._frozen = False
+        self._native = None  # cached VpbGrid (device pointers are stable until a tensor is replaced)
+        self._native_params = None
 
     # -- state access -------------------------------------------------------
     @property
@@ -108,6 +118,7 @@ class VoxelGrid:
             raise ValueError("cannot modify a frozen grid snapshot")
         self._log_odds = torch.as_tensor(value, dtype=torch.float64, device=self.device).reshape(self.dims).contiguous()
         self._bits_valid = False
+        self._native = None
 
     @property
     def observed(self) -> torch.Tensor:
@@ -170,6 +181,8 @@ class VoxelGrid:
         clone._occ_bits = self._occ_bits.clone()
         clone._bits_valid = self._bits_valid
         clone._frozen = True
+        clone._native = None
+        clone._native_params = None
         return clone
 
     def validate_box(self, box: VoxelBox) -> None:
@@ -179,6 +192,8 @@ class VoxelGrid:
 
     # -- native views ---------------------------------------------------------
     def _struct(self) -> VpbGrid:
+        if self._native is not None:
+            return self._native
         g = VpbGrid()
         g.log_odds = D.ptr(self._log_odds)
         g.observed = D.ptr(self._observed)
@@ -186,6 +201,7 @@ class VoxelGrid:
         g.dims = i64x3(self.dims)
         fill(g.origin, self.origin)
         g.voxel = self.voxel_size
+        self._native = g
         return g
 
     def _ensure_bits(self) -> None:
@@ -221,6 +237,9 @@ class CameraModel:
         return inv.rotation.matrix, inv.translation
 
     def _struct(self) -> VpbCamera:
+        cached = self.__dict__.get("_native")
+        if cached is not None:
+            return cached
         c = VpbCamera()
         c.fx, c.fy, c.cx, c.cy = self.fx, self.fy, self.cx, self.cy
         c.d_min, c.d_max = self.d_min, self.d_max
@@ -230,6 +249,7 @@ class CameraModel:
         r, t = self.world_to_camera()
         fill(c.w2c_r, r)
         fill(c.w2c_t, t)
+        object.__setattr__(self, "_native", c)  # frozen: the struct never changes
         return c
 
 
@@ -288,8 +308,10 @@ def _mask_arrays(mask):
 
 
 def _map_params(grid: VoxelGrid) -> VpbMapParams:
-    p = grid.params
-    return VpbMapParams(p.l_hit, p.l_miss, p.l_min, p.l_max, p.l_occ_threshold, grid.tau)
+    if grid._native_params is None:
+        p = grid.params
+        grid._native_params = VpbMapParams(p.l_hit, p.l_miss, p.l_min, p.l_max, p.l_occ_threshold, grid.tau)
+    return grid._native_params
 
 
 def update_occupancy(grid: VoxelGrid, depth: DepthImage, cam: CameraModel, mask=None,
@@ -313,8 +335,9 @@ def update_occupancy(grid: VoxelGrid, depth: DepthImage, cam: CameraModel, mask=
     d_dev = depth.device_tensor(dev)
     scratch = D.Workspace.get(dev, "pixel_mask", int(load().vpb_pixel_scratch_bytes(cam.width, cam.height)),
                               zeroed=True)
+    blo, bn = box.native()
     check(load().vpb_update_occupancy(
-        grid._struct(), i64x3(box.lo), i64x3(box.shape), cam._struct(), D.ptr(d_dev),
+        grid._struct(), blo, bn, cam._struct(), D.ptr(d_dev),
         D.host_ptr(centers), D.host_ptr(radii), centers.shape[0], float(mask_pad),
         _map_params(grid), D.ptr(scratch), D.stream(dev)), "update_occupancy")
     return grid
@@ -388,12 +411,12 @@ def edt_3d(grid: VoxelGrid, volume: VoxelBox | None = None, outside_default: flo
         raise ValueError(f"pass_order must permute x, y, z; got {pass_order}")
     grid._ensure_bits()
     dev = grid.device
-    n = i64x3(box.shape)
+    blo, n = box.native()
     L = load()
     ws_bytes = int(L.vpb_edt3d_workspace_bytes(n))
     ws = D.Workspace.get(dev, "edt", ws_bytes)
     out = torch.empty(box.shape, dtype=torch.float32, device=dev)
-    check(L.vpb_edt3d(grid._struct(), i64x3(box.lo), n, grid.params.l_occ_threshold, 1, D.ptr(out),
+    check(L.vpb_edt3d(grid._struct(), blo, n, grid.params.l_occ_threshold, 1, D.ptr(out),
                       D.ptr(ws), ws.numel(), D.stream(dev)), "edt_3d")
     return DistanceField(grid.origin, grid.voxel_size, grid.dims, box, out, float(outside_default))
 
