@@ -156,3 +156,79 @@ class ShardedGraph:
         self.graph.replay()
         torch.cuda.current_stream(self.pl.device).synchronize()
         return self.pl.unpack_step(self.host_out.numpy().copy(), state, goal, self.h)
+
+
+class ShardedMapper:
+    """The map side of SURVEY.md 8e, option 1: every rank keeps its own
+    replica of the occupancy grid and distance field, and per map update only
+    the source rank's input frame travels -- the depth image (160 x 120 f64 =
+    154 KB) and the body-mask spheres, in ONE broadcast of a fixed-size block.
+    Fusion and the EDT are deterministic and exact (bitwise the reference's),
+    so every replica is bit-identical and the 67 MB (256^3) / 537 MB (512^3)
+    field is never sent.  `mapper` is any object with the OccupancyMapper
+    interface (update(depth, mask=...), recompute_edt()); `cam_hw` is the
+    camera's (height, width) (known on every rank).
+
+    Block layout (float64): [H*W depth | n_mask | 3 * MAX centers | MAX radii]."""
+
+    MAX_SPHERES = 64
+
+    def __init__(self, mapper, cam_hw, world: int = 1, rank: int = 0, src: int = 0, group=None, device=None):
+        self.mapper = mapper
+        self.h, self.w = int(cam_hw[0]), int(cam_hw[1])
+        self.world, self.rank, self.src, self.group = int(world), int(rank), int(src), group
+        self.device = device
+        n = self.h * self.w + 1 + 4 * self.MAX_SPHERES
+        on_dev = device is not None and (world == 1 or dist.get_backend(group) == "nccl")
+        self._block = torch.zeros(n, dtype=torch.float64, device=device if on_dev else "cpu")
+
+    def _pack(self, depth, mask) -> None:
+        b = self._block
+        hw = self.h * self.w
+        d = depth.data if hasattr(depth, "data") and not torch.is_tensor(depth) else depth
+        d = d.reshape(-1).to(torch.float64) if torch.is_tensor(d) else np.asarray(d, dtype=np.float64).reshape(-1)
+        b[:hw] = torch.as_tensor(d, device=b.device)
+        if mask is None:
+            b[hw] = 0.0
+            return
+        centers = np.asarray(mask[0], dtype=np.float64).reshape(-1, 3)
+        radii = np.asarray(mask[1], dtype=np.float64).reshape(-1)
+        k = centers.shape[0]
+        if k > self.MAX_SPHERES or radii.shape[0] != k:
+            raise ValueError(f"mask must hold <= {self.MAX_SPHERES} spheres with one radius each")
+        b[hw] = float(k)
+        m = self.MAX_SPHERES
+        b[hw + 1:hw + 1 + 3 * k] = torch.as_tensor(centers.reshape(-1), device=b.device)
+        b[hw + 1 + 3 * m:hw + 1 + 3 * m + k] = torch.as_tensor(radii, device=b.device)
+
+    def _unpack(self):
+        b = self._block
+        hw = self.h * self.w
+        m = self.MAX_SPHERES
+        depth = b[:hw].reshape(self.h, self.w)
+        k = int(b[hw].item())
+        mask = None
+        if k > 0:
+            host = b[hw + 1:].cpu().numpy()
+            mask = (host[:3 * k].reshape(k, 3).copy(), host[3 * m:3 * m + k].copy())
+        return depth, mask
+
+    def broadcast_frame(self, depth=None, mask=None):
+        """Source rank: pack (depth, mask); every rank: receive the same block.
+        Returns this rank's (depth (H, W) f64 tensor, mask or None)."""
+        if self.rank == self.src:
+            if depth is None:
+                raise ValueError("the source rank must provide the depth frame")
+            self._pack(depth, mask)
+        if self.world > 1:
+            dist.broadcast(self._block, src=self.src, group=self.group)
+        return self._unpack()
+
+    def update(self, depth=None, mask=None) -> None:
+        """One map update on this rank's replica from the source rank's frame
+        (depth handed to the mapper as an (H, W) f64 tensor)."""
+        d, m = self.broadcast_frame(depth, mask)
+        self.mapper.update(d, mask=m)
+
+    def recompute_edt(self):
+        return self.mapper.recompute_edt()

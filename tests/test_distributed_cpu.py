@@ -8,6 +8,7 @@ the unsharded soft_weights + update_controls of the whole batch
 (vp/planner.py:373-400) on every rank, bit-identically across ranks.
 """
 
+import hashlib
 import os
 import socket
 from types import SimpleNamespace
@@ -105,3 +106,73 @@ def test_sample_range_partition(world, rank):
     sh = distributed.ShardedSMPC(SimpleNamespace(params=SimpleNamespace(samples=4096)), world=world, rank=rank)
     assert sh.global_samples == world * 4096
     assert sh.sample_range() == (rank * 4096, (rank + 1) * 4096)
+
+
+# ----------------------------------------------------------------------------- map replicas
+class _OracleMapper:
+    """OccupancyMapper stand-in on the CPU oracle (the product mapper needs a
+    GPU): masked pixels + fusion + EDT of the bench scene's grid."""
+
+    def __init__(self, n):
+        from oracle import scene as osc
+
+        self.osc = osc
+        self.cam = osc.Camera()
+        self.dims = (n, n, n)
+        extent = np.array(self.dims) * 0.02
+        self.origin = np.array([-extent[0] / 2.0, -extent[1] / 2.0, 0.0])
+        self.lo = np.zeros(self.dims)
+        self.ob = np.zeros(self.dims, bool)
+
+    def update(self, depth, mask=None):
+        depth = depth.cpu().numpy() if torch.is_tensor(depth) else np.asarray(depth)
+        c, r = mask if mask is not None else (np.zeros((0, 3)), np.zeros(0))
+        cam = self.cam
+        pm = oracle.masked_pixels(depth, cam.fx, cam.fy, cam.cx, cam.cy, cam.d_min, cam.d_max, cam.pose_r,
+                                  cam.pose_t, c, r, 0.01)
+        wr, wt = cam.world_to_camera()
+        oracle.fuse_voxels(self.lo, self.ob, (0, 0, 0), self.dims, self.origin, 0.02, wr, wt, cam.fx, cam.fy, cam.cx,
+                           cam.cy, cam.width, cam.height, cam.d_min, cam.d_max, depth, pm, c, r, 0.05, 0.85, -0.4,
+                           -2.0, 3.5)
+
+    def recompute_edt(self):
+        return oracle.edt3d(self.lo)
+
+
+def _mapper_worker(rank, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        from oracle import scene as osc
+        from paper_2512_22575_b200 import distributed
+
+        n = 48
+        frames = osc.moving_obstacle_frames((n, n, n), 3) if rank == 0 else [(None, None)] * 3
+        sm = distributed.ShardedMapper(_OracleMapper(n), (120, 160), world=WORLD, rank=rank)
+        digests = []
+        for depth, mask in frames:  # only rank 0 holds the camera frames
+            sm.update(depth, mask=mask)
+            sq = sm.recompute_edt()
+            digests.append([hashlib.sha1(a.tobytes()).hexdigest() for a in (sq, sm.mapper.lo, sm.mapper.ob)])
+        np.savez(os.path.join(out_dir, f"map{rank}.npz"), sq=sq, lo=sm.mapper.lo, digests=np.array(digests))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_mapper_replicas_bitwise_gloo(tmp_path):
+    """Rank 0 broadcasts each frame (depth + mask spheres, one block); both
+    ranks fuse and transform their own replica: bit-identical fields, and
+    equal to a single-process run on the same frames."""
+    mp.start_processes(_mapper_worker, args=(_free_port(), str(tmp_path)), nprocs=WORLD, start_method="fork")
+    r0, r1 = (np.load(tmp_path / f"map{r}.npz") for r in range(WORLD))
+    np.testing.assert_array_equal(r0["digests"], r1["digests"])
+    np.testing.assert_array_equal(r0["sq"], r1["sq"])
+    from oracle import scene as osc
+
+    ref = _OracleMapper(48)
+    for depth, mask in osc.moving_obstacle_frames((48, 48, 48), 3):
+        ref.update(depth, mask=mask)
+    np.testing.assert_array_equal(r0["sq"], ref.recompute_edt())
+    np.testing.assert_array_equal(r1["lo"], ref.lo)
+    assert np.isfinite(r0["sq"]).any() and (r0["sq"] == 0).any()
