@@ -211,8 +211,9 @@ def closed_loop(dev, dims, samples, horizon, frames, warm=3):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         mapper.update(depths[f], mask=masks[f])
-        field = mapper.recompute_edt()
-        res = pl.smpc_step(state, goal, field, nominal, f)
+        mapper.recompute_edt()
+        snap = mapper.snapshot()  # inside map_ms like vp/sim.py:476-480 (O(1): copy-on-write)
+        res = pl.smpc_step(state, goal, snap, nominal, f)
         e1.record(stream)
         e1.synchronize()
         if f >= warm:
@@ -223,7 +224,8 @@ def closed_loop(dev, dims, samples, horizon, frames, warm=3):
             "p90": float(np.percentile(times, 90)), "frames": frames, "grid": list(dims), "samples": samples,
             "horizon": horizon,
             "per_frame": "masked fusion (160x120 depth, 11-sphere body mask) + exact EDT of the whole grid + "
-                         "Planner.smpc_step (host in/out); depth rendered on the host, untimed"}
+                         "mapper.snapshot() + Planner.smpc_step on the snapshot (host in/out); depth rendered on "
+                         "the host, untimed"}
 
 
 # ----------------------------------------------------------------------------- ours

@@ -110,6 +110,41 @@ int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3],
                          const vpb_map_params *params, uint8_t *pixel_scratch,
                          void *stream);
 
+/* Snapshot journal (copy-on-write snapshots of a live grid, vp/mapping.py
+ * :125-133 freeze / :713-723 snapshot): while a snapshot of the grid is alive,
+ * each update records, before its first write to a 32-voxel word, the word's
+ * old log-odds and observed (all 32 z) and its old occupancy word.  A
+ * snapshot is then O(1); it is materialised (clone + these undo records,
+ * newest update first) only if its grid is read.  All buffers (dev) are
+ * caller-owned; count (dev) is the number of records written, capacity the
+ * records the buffers hold (the host sizes it so one update cannot overflow:
+ * at most one record per word of the box). */
+typedef struct {
+  int64_t *idx;              /* [capacity] word (x * Ny + y) * ceil(Nz / 32) + z / 32 */
+  double *lo;                /* [capacity * 32] old log-odds of the word's z */
+  uint8_t *ob;               /* [capacity * 32] old observed */
+  uint32_t *occ;             /* [capacity] old occupancy word */
+  unsigned long long *count; /* records written (dev) */
+  unsigned int *overflow;    /* set if a record did not fit (dev) */
+  uint64_t capacity;
+} vpb_journal;
+
+/* vpb_update_occupancy that also journals the words it modifies
+ * (journal == NULL: identical to vpb_update_occupancy). */
+int vpb_update_occupancy_journaled(const vpb_grid *grid, const int64_t lo[3],
+                                   const int64_t n[3], const vpb_camera *cam,
+                                   const double *depth, const double *centers,
+                                   const double *radii, int64_t n_mask,
+                                   double mask_pad,
+                                   const vpb_map_params *params,
+                                   uint8_t *pixel_scratch,
+                                   const vpb_journal *journal, void *stream);
+
+/* Undo records [first, last) of one update (unique words) written back into
+ * grid (a clone of the live grid); call per update, newest first. */
+int vpb_journal_restore(const vpb_grid *grid, const vpb_journal *journal,
+                        int64_t first, int64_t last, void *stream);
+
 /* Exact squared EDT of the occupied voxels of box [lo, lo+n).
  * Replaces the body of vp/mapping.py:586-613 (edt_3d: threshold, the three
  * _edt_pass_* FH passes of :458-550, and the inf mapping).  Output out_sq

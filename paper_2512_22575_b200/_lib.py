@@ -53,6 +53,11 @@ class VpbGrid(ctypes.Structure):
                 ("origin", _d * 3), ("voxel", _d)]
 
 
+class VpbJournal(ctypes.Structure):
+    _fields_ = [("idx", _p), ("lo", _p), ("ob", _p), ("occ", _p), ("count", _p), ("overflow", _p),
+                ("capacity", ctypes.c_uint64)]
+
+
 class VpbField(ctypes.Structure):
     _fields_ = [("sq", _p), ("n", _i64 * 3), ("lo", _i64 * 3), ("origin", _d * 3), ("voxel", _d),
                 ("outside_default", _d)]
@@ -93,6 +98,9 @@ SIGNATURES = {
                                        _i64, _P(VpbMapParams), _p]),
     "vpb_update_occupancy": (ctypes.c_int, [_P(VpbGrid), _P(_i64), _P(_i64), _P(VpbCamera), _p, _p, _p,
                                             _i64, _d, _P(VpbMapParams), _p, _p]),
+    "vpb_update_occupancy_journaled": (ctypes.c_int, [_P(VpbGrid), _P(_i64), _P(_i64), _P(VpbCamera), _p, _p,
+                                                      _p, _i64, _d, _P(VpbMapParams), _p, _P(VpbJournal), _p]),
+    "vpb_journal_restore": (ctypes.c_int, [_P(VpbGrid), _P(VpbJournal), _i64, _i64, _p]),
     "vpb_edt3d_workspace_bytes": (_sz, [_P(_i64)]),
     "vpb_edt3d": (ctypes.c_int, [_P(VpbGrid), _P(_i64), _P(_i64), _d, ctypes.c_int, _p, _p, _sz, _p]),
     "vpb_query_distance": (ctypes.c_int, [_P(VpbField), _p, _i64, _p, _p]),

@@ -45,6 +45,7 @@ struct FusionArgs {
   // rotation, voxel-index box of the mask spheres (empty if none)
   float camc[3], c2w[9];
   int mask_i_lo[3], mask_i_hi[3];
+  vpb_journal journal;  // undo records of the modified words (journal.idx == null: off)
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr2[VPB_MAX_MASK_SPHERES];
 };
@@ -54,9 +55,9 @@ __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a,
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 
 // Exact fp64 restatement of one voxel's update (vp/mapping.py:300-354), the
-// reference's operations in its order.  Returns true if the voxel was
-// written; *newval receives its log-odds.  Kept out of line so the fp32
-// prefilter loop stays small.
+// reference's operations in its order.  Returns true if the voxel is
+// touched (observed becomes 1); *newval receives its new log-odds (the caller
+// writes both).  Kept out of line so the fp32 prefilter loop stays small.
 __device__ __noinline__ bool exact_voxel(const FusionArgs &A, int64_t x, int64_t y, int64_t z, int64_t g,
                                          double *newval) {
   const double px = dadd(A.origin0, dmul(dadd((double)x, 0.5), A.voxel));
@@ -73,8 +74,6 @@ __device__ __noinline__ bool exact_voxel(const FusionArgs &A, int64_t x, int64_t
       if (d2 < A.mr2[s]) {
         const double old = A.log_odds[g];
         *newval = old > 0.0 ? 0.0 : old;
-        if (old > 0.0) A.log_odds[g] = 0.0;
-        A.observed[g] = 1;
         return true;
       }
     }
@@ -100,8 +99,6 @@ __device__ __noinline__ bool exact_voxel(const FusionArgs &A, int64_t x, int64_t
   double value = dadd(A.log_odds[g], cls == 1 ? A.l_hit : A.l_miss);
   if (value < A.l_min) value = A.l_min;
   else if (value > A.l_max) value = A.l_max;
-  A.log_odds[g] = value;
-  A.observed[g] = 1;
   *newval = value;
   return true;
 }
@@ -360,28 +357,46 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
       }
       bool touched = false;
       double newval = 0.0;
+      const int64_t g = gline + z;
       if (fast) {
         // certain hit / miss: the reference's fp64 update, bit for bit
-        const int64_t g = gline + z;
         double value = dadd(A.log_odds[g], fast == 1 ? A.l_hit : A.l_miss);
         if (value < A.l_min) value = A.l_min;
         else if (value > A.l_max) value = A.l_max;
-        A.log_odds[g] = value;
-        A.observed[g] = 1;
         newval = value;
         touched = true;
       } else if (exact) {
-        touched = exact_voxel(A, x, y, z, gline + z, &newval);
+        touched = exact_voxel(A, x, y, z, g, &newval);
       }
-      if (A.occ_bits != nullptr) {
-        const unsigned touched_mask = __ballot_sync(kFull, touched);
-        if (touched_mask != 0u) {
-          const unsigned occ_mask = __ballot_sync(kFull, touched && newval >= A.l_thr);
+      const unsigned touched_mask = __ballot_sync(kFull, touched);
+      if (touched_mask == 0u) continue;
+      uint32_t *ow = A.occ_bits != nullptr ? A.occ_bits + (x * A.gy + y) * A.words_z + wz : nullptr;
+      if (A.journal.idx != nullptr) {
+        // undo record of this word before its first write (snapshot journal):
+        // the old log-odds / observed of all 32 z and the old occupancy word
+        unsigned long long slot = 0;
+        if (lane == 0) slot = atomicAdd(A.journal.count, 1ull);
+        slot = __shfl_sync(kFull, slot, 0);
+        if (slot < A.journal.capacity) {
+          const bool inz = z < A.gz;
+          A.journal.lo[slot * 32 + lane] = inz ? A.log_odds[g] : 0.0;
+          A.journal.ob[slot * 32 + lane] = inz ? A.observed[g] : 0;
           if (lane == 0) {
-            uint32_t *w = A.occ_bits + (x * A.gy + y) * A.words_z + wz;
-            *w = (*w & ~touched_mask) | (occ_mask & touched_mask);
+            A.journal.idx[slot] = (x * A.gy + y) * A.words_z + wz;  // word index of the grid
+            A.journal.occ[slot] = ow ? *ow : 0u;
           }
+        } else if (lane == 0) {
+          atomicOr(A.journal.overflow, 1u);  // (the host sizes the journal so this cannot happen)
         }
+        __syncwarp();
+      }
+      if (touched) {
+        A.log_odds[g] = newval;
+        A.observed[g] = 1;
+      }
+      if (ow != nullptr) {
+        const unsigned occ_mask = __ballot_sync(kFull, touched && newval >= A.l_thr);
+        if (lane == 0) *ow = (*ow & ~touched_mask) | (occ_mask & touched_mask);
       }
     }
   }
@@ -505,6 +520,29 @@ __global__ void __launch_bounds__(256) occ_bits_kernel(const double *__restrict_
   if (lane == 0) bits[w] = m;
 }
 
+// One warp per undo record: the word's 32 old log-odds / observed and its
+// old occupancy word back into the clone.
+__global__ void __launch_bounds__(256) journal_restore_kernel(double *__restrict__ log_odds,
+                                                              uint8_t *__restrict__ observed,
+                                                              uint32_t *__restrict__ occ_bits, int64_t gz,
+                                                              int64_t words_z, const int64_t *__restrict__ idx,
+                                                              const double *__restrict__ jlo,
+                                                              const uint8_t *__restrict__ job,
+                                                              const uint32_t *__restrict__ jocc, int64_t first,
+                                                              int64_t last) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = first + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= last) return;
+  const int64_t w = idx[r];
+  const int64_t line = w / words_z, wz = w - line * words_z;
+  const int64_t z = wz * 32 + lane;
+  if (z < gz) {
+    log_odds[line * gz + z] = jlo[r * 32 + lane];
+    observed[line * gz + z] = job[r * 32 + lane];
+  }
+  if (lane == 0 && occ_bits) occ_bits[w] = jocc[r];
+}
+
 }  // namespace vpb
 
 using namespace vpb;
@@ -579,7 +617,7 @@ static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const 
 static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
                      const double *depth, const uint8_t *pixel_masked, const double *centers,
                      const double *radii, int64_t n_mask, const vpb_map_params *p, int usable, const int *bbox,
-                     void *stream) {
+                     void *stream, const vpb_journal *journal = nullptr) {
   VPB_REQUIRE(grid && grid->log_odds && grid->observed && cam && depth && pixel_masked && p,
               "null argument to vpb_fuse_voxels");
   for (int k = 0; k < 3; ++k)
@@ -592,6 +630,11 @@ static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
   A.log_odds = grid->log_odds;
   A.observed = grid->observed;
   A.occ_bits = grid->occ_bits;
+  if (journal) {
+    VPB_REQUIRE(journal->idx && journal->lo && journal->ob && journal->occ && journal->count && journal->overflow,
+                "incomplete snapshot journal");
+    A.journal = *journal;
+  }
   A.gy = grid->dims[1];
   A.gz = grid->dims[2];
   A.words_z = ceil_div(grid->dims[2], 32);
@@ -681,6 +724,15 @@ int64_t vpb_pixel_scratch_bytes(int64_t width, int64_t height) {
 int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
                          const double *depth, const double *centers, const double *radii, int64_t n_mask,
                          double mask_pad, const vpb_map_params *params, uint8_t *pixel_scratch, void *stream) {
+  return vpb_update_occupancy_journaled(grid, lo, n, cam, depth, centers, radii, n_mask, mask_pad, params,
+                                        pixel_scratch, nullptr, stream);
+}
+
+int vpb_update_occupancy_journaled(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3],
+                                   const vpb_camera *cam, const double *depth, const double *centers,
+                                   const double *radii, int64_t n_mask, double mask_pad,
+                                   const vpb_map_params *params, uint8_t *pixel_scratch, const vpb_journal *journal,
+                                   void *stream) {
   VPB_REQUIRE(pixel_scratch, "pixel scratch is null");
   // pixel classes in one byte: 1 = return on the robot body, 2 = usable
   // return; followed by the bounding rectangle of the usable pixels
@@ -688,7 +740,18 @@ int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3], const int64_
   int *bbox = reinterpret_cast<int *>(pixel_scratch + align_up((size_t)npx, 16));
   int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, bbox, stream);
   if (rc) return rc;
-  return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, bbox, stream);
+  return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, bbox, stream, journal);
+}
+
+int vpb_journal_restore(const vpb_grid *grid, const vpb_journal *j, int64_t first, int64_t last, void *stream) {
+  VPB_REQUIRE(grid && grid->log_odds && grid->observed && j && j->idx && j->lo && j->ob && j->occ,
+              "null argument to vpb_journal_restore");
+  VPB_REQUIRE(first >= 0 && first <= last && (uint64_t)last <= j->capacity, "journal range outside capacity");
+  if (last == first) return VPB_OK;
+  journal_restore_kernel<<<(unsigned)ceil_div(last - first, 8), 256, 0, as_stream(stream)>>>(
+      grid->log_odds, grid->observed, grid->occ_bits, grid->dims[2], ceil_div(grid->dims[2], 32), j->idx, j->lo,
+      j->ob, j->occ, first, last);
+  return check_launch("journal_restore_kernel");
 }
 
 }  // extern "C"

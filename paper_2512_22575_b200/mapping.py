@@ -11,6 +11,7 @@ occupancy mask packs z into 32-bit words per (x, y) line.
 
 from __future__ import annotations
 
+import weakref
 from dataclasses import dataclass, field as dc_field
 from enum import IntEnum
 
@@ -18,7 +19,7 @@ import numpy as np
 import torch
 
 from . import _device as D
-from ._lib import VpbCamera, VpbField, VpbGrid, VpbMapParams, check, fill, i64x3, load
+from ._lib import VpbCamera, VpbField, VpbGrid, VpbJournal, VpbMapParams, check, fill, i64x3, load
 from .errors import FrameMismatch, VolumeOutOfBounds
 from .geometry import RigidTransform
 
@@ -104,24 +105,30 @@ class VoxelGrid:
         self._frozen = False
         self._native = None  # cached VpbGrid (device pointers are stable until a tensor is replaced)
         self._native_params = None
+        self._snaps: list = []  # weakrefs to the live (unmaterialised) snapshots of this grid
+        self._journal = None
 
     # -- state access -------------------------------------------------------
     @property
     def log_odds(self) -> torch.Tensor:
         if not self._frozen:
-            self._bits_valid = False  # caller may write through this handle
+            self._detach_snapshots()  # the caller may write through this handle
+            self._bits_valid = False
         return self._log_odds
 
     @log_odds.setter
     def log_odds(self, value) -> None:
         if self._frozen:
             raise ValueError("cannot modify a frozen grid snapshot")
+        self._detach_snapshots()
         self._log_odds = torch.as_tensor(value, dtype=torch.float64, device=self.device).reshape(self.dims).contiguous()
         self._bits_valid = False
         self._native = None
 
     @property
     def observed(self) -> torch.Tensor:
+        if not self._frozen:
+            self._detach_snapshots()  # a writable view
         return self._observed.view(torch.bool)
 
     def log_odds_host(self) -> np.ndarray:
@@ -138,6 +145,7 @@ class VoxelGrid:
         """log_odds[mask] = value (default l_max), like `grid.log_odds[occ] = l_max`."""
         if self._frozen:
             raise ValueError("cannot modify a frozen grid snapshot")
+        self._detach_snapshots()
         m = torch.as_tensor(np.asarray(mask, dtype=bool) if not torch.is_tensor(mask) else mask,
                             device=self.device)
         self._log_odds[m] = self.params.l_max if value is None else float(value)
@@ -169,21 +177,52 @@ class VoxelGrid:
         return out
 
     def freeze(self) -> "VoxelGrid":
-        """Deep immutable copy in device memory (vp/mapping.py:125-133)."""
-        clone = VoxelGrid.__new__(VoxelGrid)
-        clone.device = self.device
-        clone.origin = self.origin.copy()
-        clone.voxel_size = self.voxel_size
-        clone.dims = self.dims
-        clone.params = self.params
-        clone._log_odds = self._log_odds.clone()
-        clone._observed = self._observed.clone()
-        clone._occ_bits = self._occ_bits.clone()
-        clone._bits_valid = self._bits_valid
-        clone._frozen = True
-        clone._native = None
-        clone._native_params = None
-        return clone
+        """Immutable snapshot (vp/mapping.py:125-133) in O(1): a copy-on-write
+        view.  While it is alive, every fusion into this grid journals the
+        words it modifies (old values, on the device); the snapshot's own
+        state is materialised -- clone of the live grid + the undo records,
+        newest update first -- only if it is ever read.  A snapshot that is
+        dropped unread (the planner reads only the field) never costs a copy."""
+        if self._frozen:
+            return self
+        snap = SnapshotGrid(self)
+        self._snaps.append(weakref.ref(snap))
+        return snap
+
+    # -- copy-on-write snapshots ------------------------------------------------
+    def _live_snaps(self) -> list:
+        live = [r() for r in self._snaps]
+        live = [g for g in live if g is not None and g._state is None]
+        self._snaps = [weakref.ref(g) for g in live]
+        return live
+
+    def _detach_snapshots(self) -> None:
+        """Before an unjournaled in-place change: give every live snapshot its own state."""
+        for g in self._live_snaps():
+            g._materialize()
+        self._snaps = []
+        if self._journal is not None:
+            self._journal.reset()
+
+    def _journal_for_update(self, box: "VoxelBox"):
+        """The journal struct for the next fusion (None if no snapshot is alive)."""
+        live = self._live_snaps()
+        j = self._journal
+        if not live:
+            if j is not None:
+                j.reset()
+            return None
+        if j is None:
+            j = self._journal = _Journal(self)
+        if min(g._seg for g in live) == j.nseg:  # nothing journaled so far is still needed
+            j.reset()
+            for g in live:
+                g._seg = 0
+        words = box.shape[0] * box.shape[1] * ((box.hi[2] - 1) // 32 - box.lo[2] // 32 + 1)
+        if j.nseg == _Journal.MAX_SEG:  # a snapshot outlived too many updates: give it its own state
+            self._detach_snapshots()
+            return None
+        return j.begin_segment(words)
 
     def validate_box(self, box: VoxelBox) -> None:
         for axis in range(3):
@@ -210,6 +249,123 @@ class VoxelGrid:
             check(load().vpb_occ_bits_from_log_odds(g, self.params.l_occ_threshold, D.stream(self.device)),
                   "occupancy mask")
             self._bits_valid = True
+
+
+class _Journal:
+    """Undo records of one live grid (include/vpb200.h vpb_journal): device
+    buffers grown on demand, one segment per journaled update."""
+
+    MAX_SEG = 16
+    RECORD_BYTES = 8 + 32 * 8 + 32 + 4
+
+    def __init__(self, grid: VoxelGrid):
+        self.dev = grid.device
+        self.cap = 0
+        self.bound = 0  # host upper bound of the records written (one per box word per update)
+        self.nseg = 0
+        self.count = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self.overflow = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        self.starts = torch.zeros(self.MAX_SEG, dtype=torch.int64, device=self.dev)
+        self.idx = self.lo = self.ob = self.occ = None
+        self._struct = None
+
+    def reset(self) -> None:
+        if self.nseg or self.bound:
+            self.count.zero_()
+        self.nseg = 0
+        self.bound = 0
+
+    def _grow(self, cap: int) -> None:
+        new = (torch.empty(cap, dtype=torch.int64, device=self.dev),
+               torch.empty(cap * 32, dtype=torch.float64, device=self.dev),
+               torch.empty(cap * 32, dtype=torch.uint8, device=self.dev),
+               torch.empty(cap, dtype=torch.int32, device=self.dev))
+        if self.idx is not None and self.bound:
+            keep = min(self.bound, self.cap)
+            for a, b, k in zip(new, (self.idx, self.lo, self.ob, self.occ), (1, 32, 32, 1)):
+                a[:keep * k].copy_(b[:keep * k])
+        self.idx, self.lo, self.ob, self.occ = new
+        self.cap = cap
+        j = VpbJournal()
+        j.idx, j.lo, j.ob, j.occ = (D.ptr(t) for t in new)
+        j.count, j.overflow, j.capacity = D.ptr(self.count), D.ptr(self.overflow), cap
+        self._struct = j
+
+    def begin_segment(self, words: int) -> VpbJournal:
+        if self.bound + words > self.cap:
+            self._grow(max(2 * self.cap, self.bound + words))
+        self.starts[self.nseg:self.nseg + 1].copy_(self.count)  # device-side: no sync
+        self.nseg += 1
+        self.bound += words
+        return self._struct
+
+    def restore_into(self, grid: "SnapshotGrid", first_seg: int) -> None:
+        """Write the undo records of segments nseg-1 .. first_seg (newest first) into grid."""
+        if first_seg >= self.nseg:
+            return
+        ends = torch.cat([self.starts[:self.nseg], self.count]).cpu().numpy()
+        if int(self.overflow.item()):
+            raise RuntimeError("snapshot journal overflow (sizing bug)")
+        L = load()
+        st = grid._struct()
+        for k in range(self.nseg - 1, first_seg - 1, -1):
+            check(L.vpb_journal_restore(st, self._struct, int(ends[k]), int(ends[k + 1]), D.stream(self.dev)),
+                  "journal_restore")
+
+
+class SnapshotGrid(VoxelGrid):
+    """Frozen VoxelGrid produced by VoxelGrid.freeze(): reads materialise it."""
+
+    def __init__(self, live: VoxelGrid):  # noqa: D401 - no VoxelGrid.__init__ (no allocation)
+        self.device = live.device
+        self.origin = live.origin.copy()
+        self.voxel_size = live.voxel_size
+        self.dims = live.dims
+        self.params = live.params
+        self._frozen = True
+        self._native = None
+        self._native_params = None
+        self._snaps = []
+        self._journal = None
+        self._live = live
+        self._seg = live._journal.nseg if live._journal is not None else 0
+        self._bits_at_freeze = live._bits_valid
+        self._state = None  # (log_odds, observed, occ_bits) once materialised
+
+    def _materialize(self):
+        if self._state is None:
+            live = self._live
+            state = (live._log_odds.clone(), live._observed.clone(), live._occ_bits.clone())
+            self._state = state
+            if live._journal is not None:
+                live._journal.restore_into(self, self._seg)
+            self._live = None
+        return self._state
+
+    @property
+    def _log_odds(self):
+        return self._materialize()[0]
+
+    @property
+    def _observed(self):
+        return self._materialize()[1]
+
+    @property
+    def _occ_bits(self):
+        return self._materialize()[2]
+
+    @property
+    def _bits_valid(self):
+        return self._bits_at_freeze
+
+    @_bits_valid.setter
+    def _bits_valid(self, value):
+        self._bits_at_freeze = value
+
+    def _struct(self) -> VpbGrid:
+        if self._state is None:  # restore needs the clone's pointers: materialise first
+            self._materialize()
+        return VoxelGrid._struct(self)
 
 
 @dataclass(frozen=True)
@@ -336,10 +492,11 @@ def update_occupancy(grid: VoxelGrid, depth: DepthImage, cam: CameraModel, mask=
     scratch = D.Workspace.get(dev, "pixel_mask", int(load().vpb_pixel_scratch_bytes(cam.width, cam.height)),
                               zeroed=True)
     blo, bn = box.native()
-    check(load().vpb_update_occupancy(
+    journal = grid._journal_for_update(box) if grid._snaps else None
+    check(load().vpb_update_occupancy_journaled(
         grid._struct(), blo, bn, cam._struct(), D.ptr(d_dev),
         D.host_ptr(centers), D.host_ptr(radii), centers.shape[0], float(mask_pad),
-        _map_params(grid), D.ptr(scratch), D.stream(dev)), "update_occupancy")
+        _map_params(grid), D.ptr(scratch), journal, D.stream(dev)), "update_occupancy")
     return grid
 
 

@@ -67,7 +67,7 @@ def test_struct_layout_matches_header(lib):
     import subprocess, tempfile
     from paper_2512_22575_b200 import _lib
 
-    src = '#include <stdio.h>\n#include "vpb200.h"\nint main(){printf("%zu %zu %zu %zu %zu\\n", sizeof(vpb_camera), sizeof(vpb_map_params), sizeof(vpb_grid), sizeof(vpb_field), sizeof(vpb_problem));}'
+    src = '#include <stdio.h>\n#include "vpb200.h"\nint main(){printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(vpb_camera), sizeof(vpb_map_params), sizeof(vpb_grid), sizeof(vpb_field), sizeof(vpb_problem), sizeof(vpb_journal));}'
     with tempfile.TemporaryDirectory() as d:
         c = Path(d) / "probe.c"
         c.write_text(src)
@@ -76,7 +76,8 @@ def test_struct_layout_matches_header(lib):
         if r.returncode != 0:
             pytest.skip("no C compiler")
         sizes = [int(v) for v in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
-    want = [ctypes.sizeof(t) for t in (_lib.VpbCamera, _lib.VpbMapParams, _lib.VpbGrid, _lib.VpbField, _lib.VpbProblem)]
+    want = [ctypes.sizeof(t) for t in (_lib.VpbCamera, _lib.VpbMapParams, _lib.VpbGrid, _lib.VpbField, _lib.VpbProblem,
+                                       _lib.VpbJournal)]
     assert sizes == want
 
 

@@ -380,3 +380,55 @@ def test_mapper_pipeline_512_c5_frames(M):
         field = mapper.recompute_edt()
         assert np.array_equal(field.sq_device.cpu().numpy().astype(np.float64), oracle.edt3d(lo)), f"frame {f}: EDT"
     assert ob.sum() > 100000
+
+
+def test_snapshot_copy_on_write(M):
+    """O(1) snapshots (vp/mapping.py:125-133, 713-723 semantics): each snapshot
+    keeps the state of the moment it was taken, bitwise, across later journaled
+    fusions, an unjournaled in-place write and a dropped sibling snapshot; its
+    EDT equals the oracle's on that state."""
+    from paper_2512_22575_b200 import scene
+
+    n = 96
+    grid, cam, _ = scene.bench_edt_scene((n, n, n))
+    mapper = M.OccupancyMapper(grid, cam, outside_default=0.8)
+    frames = scene.moving_obstacle_frames(cam, (n, n, n), 8)
+    want, snaps = [], []
+    for f, (depth, mask) in enumerate(frames[:6]):
+        mapper.update(M.DepthImage(depth), mask=mask)
+        mapper.recompute_edt()
+        if f in (1, 3, 4):
+            snaps.append(mapper.snapshot())
+            want.append((grid.log_odds_host().copy(), grid.observed_host().copy()))
+    j = grid._journal
+    assert j is not None and j.nseg >= 2  # the updates after the first snapshot were journaled
+    del snaps[2], want[2]  # a dropped snapshot
+    grid.mark_occupied(np.zeros(grid.dims, bool) | (np.arange(n)[:, None, None] == 3))  # unjournaled write
+    for depth, mask in frames[6:]:
+        mapper.update(M.DepthImage(depth), mask=mask)
+    for s, (lo, ob) in zip(snaps, want):
+        assert np.array_equal(s.grid.log_odds_host(), lo)
+        assert np.array_equal(s.grid.observed_host(), ob)
+        assert np.array_equal(M.edt_3d(s.grid).sq, oracle.edt3d(lo))
+        with pytest.raises(ValueError):
+            M.update_occupancy(s.grid, M.DepthImage(frames[0][0]), cam)
+    assert not np.array_equal(grid.log_odds_host(), want[-1][0])
+
+
+def test_snapshot_journal_stays_bounded(M):
+    """The closed-loop pattern (snap = mapper.snapshot() every frame, the old
+    one dropped): one journal segment at a time, never a materialisation."""
+    from paper_2512_22575_b200 import scene
+
+    n = 64
+    grid, cam, _ = scene.bench_edt_scene((n, n, n))
+    mapper = M.OccupancyMapper(grid, cam, outside_default=0.8)
+    snap = None
+    for depth, mask in scene.moving_obstacle_frames(cam, (n, n, n), 6):
+        mapper.update(M.DepthImage(depth), mask=mask)
+        mapper.recompute_edt()
+        snap = mapper.snapshot()
+        assert grid._journal is None or grid._journal.nseg <= 1
+    assert snap.grid._state is None  # never read: never copied
+    lo = grid.log_odds_host().copy()
+    assert np.array_equal(snap.grid.log_odds_host(), lo)
