@@ -145,8 +145,8 @@ def cpu_model() -> str:
 
 def ncu_traffic() -> dict:
     """DRAM bytes per launch of the step's kernels from the committed ncu
-    capture (profiles/r1_ncu_traffic.json, tools/ncu_traffic.py)."""
-    p = ROOT / "profiles" / "r1_ncu_traffic.json"
+    capture (profiles/ncu_traffic.json, tools/ncu_traffic.py)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
         return {k: v["bytes"] for k, v in json.loads(p.read_text()).items()}
     return {}
@@ -481,7 +481,7 @@ def run_ours(args):
                          "note": "FP32-issue-bound: achieved = (2294 FLOP/rollout-step x H + 1217/rollout) x M "
                                  "(SURVEY.md 8d) / CUDA-event time of one fused launch, L2 flushed; peak = SMs x "
                                  "128 x 2 x sm_max_mhz (no FP32 entry in MEASURED_PEAKS.json); traffic = ncu "
-                                 "dram__bytes_read+write of the kernel (profiles/r1_ncu_traffic.json)"},
+                                 "dram__bytes_read+write of the kernel (profiles/ncu_traffic.json)"},
             "rooflines": [
                 {"kernel": "rollout_kernel (evaluate_batch alone)", "bound": "fp32", "achieved": roll_tflops,
                  "peak": fp32_peak, "unit": "TFLOP/s", "frac": roll_tflops / fp32_peak, "ms": ms_roll},

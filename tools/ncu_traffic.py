@@ -1,6 +1,6 @@
 """DRAM traffic per launch from an ncu --set full report -> profiles JSON.
 
-    python tools/ncu_traffic.py gpurun_out/a.ncu-rep [b.ncu-rep ...] profiles/r1_ncu_traffic.json
+    python tools/ncu_traffic.py gpurun_out/a.ncu-rep [b.ncu-rep ...] profiles/ncu_traffic.json
 
 Groups launches by kernel family (smpc_kernel, edt = line table + Z+Y + X
 passes, fuse_kernel, ...) and records dram__bytes_read.sum +
