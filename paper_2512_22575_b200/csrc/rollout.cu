@@ -433,7 +433,10 @@ constexpr int smpc_threads() {
 // 4096-candidate step runs in a single wave on 148 SMs.
 template <typename T, typename Topo>
 constexpr int smpc_min_blocks() {
-  return sizeof(T) == 8 ? 1 : (is_dyn_v<Topo> ? 2 : 7);
+#ifndef VPB_SMPC_MINB
+#define VPB_SMPC_MINB 7
+#endif
+  return sizeof(T) == 8 ? 1 : (is_dyn_v<Topo> ? 2 : VPB_SMPC_MINB);
 }
 
 // One fixed-topology evaluation per warp, lane = step.  The warp integrates
@@ -1903,6 +1906,9 @@ static int set_smem(K kern, size_t smem) {
 
 template <typename T, typename ET>
 static int launch_rollout_t(const Prob<T> &P, const RolloutIO &io, int topo, cudaStream_t s) {
+#ifdef VPB_QUICK  // SASS-inspection builds (tools/quick_sass.sh): the production smpc kernel only
+  return VPB_ERR_ARG;
+#endif
   const size_t smem = smem_bytes(P, 0, topo);
   const unsigned grid = (unsigned)ceil_div(io.M, NW);
   if (grid == 0) return VPB_OK;
@@ -1957,6 +1963,15 @@ static int launch_smpc_t(const Prob<T> &P, const SmpcIO &io, int topo, cudaStrea
     io2.max_helpers = slots - 2 < kMergeHelpers ? (slots - 2 > 0 ? slots - 2 : 0) : kMergeHelpers;
     k<<<(unsigned)ctas, threads, smem, s>>>(P, io2);
   };
+#ifdef VPB_QUICK
+  if constexpr (!std::is_same_v<T, float> || !std::is_same_v<ET, float>) return VPB_ERR_ARG;
+  else {
+    auto k = smpc_kernel<T, ET, 8, TopoRobot7>;
+    if ((rc = set_smem(k, smem))) return rc;
+    go(k, smpc_threads<TopoRobot7>());
+    return check_launch("smpc_kernel");
+  }
+#endif
   if (topo == 1) {
     auto k = smpc_kernel<T, ET, 8, TopoRobot7>;
     if ((rc = set_smem(k, smem))) return rc;
@@ -1977,6 +1992,9 @@ template <typename T>
 static int launch_finish_t(const Prob<T> &P, const double *parts, int n_parts, double lam, const double *nominal,
                            const AccLimit &acc, double *merged, double *out, const double *dyn, int topo,
                            cudaStream_t s) {
+#ifdef VPB_QUICK
+  return VPB_ERR_ARG;
+#endif
   const size_t smem = smem_bytes(P, n_parts + 512, topo);
   int rc;
   if (topo == 1) {

@@ -86,8 +86,31 @@ __device__ __forceinline__ double tsqrt<double>(double x) { return sqrt(x); }
 
 template <typename T>
 __device__ __forceinline__ void tsincos(T x, T *s, T *c);
+// fp32 sin/cos without sincosf's Payne-Hanek slow path (a local-memory loop
+// behind a branch for |x| >= 105615, which the unrolled FK would carry eight
+// times per step): Cody-Waite reduction by pi/2 in three parts and the
+// classic minimax polynomials on [-pi/4, pi/4] (about 1 ulp for the joint
+// angles a rollout produces; accuracy only degrades, without branching, for
+// |x| beyond ~1e5).
 template <>
-__device__ __forceinline__ void tsincos<float>(float x, float *s, float *c) { sincosf(x, s, c); }
+__device__ __forceinline__ void tsincos<float>(float x, float *s, float *c) {
+  const float j = rintf(x * 0.636619772367581343f);
+  const int q = (int)j;
+  float r = fmaf(j, -1.57079625129699707031f, x);
+  r = fmaf(j, -7.54978941586159635335e-08f, r);
+  r = fmaf(j, -5.39030253145912640453e-15f, r);
+  const float z = r * r;
+  float ps = fmaf(-1.9515295891e-4f, z, 8.3321608736e-3f);
+  ps = fmaf(ps, z, -1.6666654611e-1f);
+  const float sn = fmaf(ps * z, r, r);
+  float pc = fmaf(2.443315711809948e-5f, z, -1.388731625493765e-3f);
+  pc = fmaf(pc, z, 4.166664568298827e-2f);
+  const float cs = fmaf(pc * z, z, fmaf(-0.5f, z, 1.0f));
+  const float s0 = (q & 1) ? cs : sn;
+  const float c0 = (q & 1) ? sn : cs;
+  *s = (q & 2) ? -s0 : s0;
+  *c = ((q + 1) & 2) ? -c0 : c0;
+}
 template <>
 __device__ __forceinline__ void tsincos<double>(double x, double *s, double *c) { sincos(x, s, c); }
 

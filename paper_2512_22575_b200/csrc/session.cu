@@ -10,6 +10,7 @@
 // device buffers (allocated once at creation), so a step does no allocation,
 // no attribute setting and no per-kernel host work.
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "vpb_common.cuh"
@@ -50,12 +51,14 @@ void release(vpb_smpc_session *s) {
 
 int enqueue(vpb_smpc_session *s, bool copies) {
   const int64_t nom = s->dyn_len + 2;
-  if (copies)
+  // (VPB_SESSION_AB: 1 = no H2D node, 2 = no host result, for overhead A/B only)
+  static const int ab = getenv("VPB_SESSION_AB") ? atoi(getenv("VPB_SESSION_AB")) : 0;
+  if (copies && ab != 1)
     VPB_CUDA(cudaMemcpyAsync(s->d_in, s->h_in, (size_t)s->in_len * 8, cudaMemcpyHostToDevice, s->stream));
   // the step kernel writes the result straight into the pinned host buffer
   return vpb::smpc_generate_session(&s->prob, &s->field, reinterpret_cast<const uint64_t *>(s->d_in + s->dyn_len),
                                     s->window, s->sigma, s->d_in + nom, s->M, s->precision, s->eps, s->d_out,
-                                    s->h_out, s->ws, s->ws_bytes, s->stream);
+                                    ab == 2 ? nullptr : s->h_out, s->ws, s->ws_bytes, s->stream);
 }
 
 // 3x3 row-major helpers (host, double)
