@@ -824,6 +824,12 @@ struct SmpcIO {
   double *out_host;  // optional host-mapped copy of `out` (+ 1 slot: the done flag), written by the last CTA
   double *cand_terms;  // [M][6] per-candidate sums (fixed path): the re-evaluation shortcut
   int max_helpers;     // helper CTAs of the heavy merge (residency-capped, see merge_helpers)
+  // session staging (fixed path): block 0 copies the host-mapped per-call
+  // block into its device copy and raises the staging word; every other CTA
+  // waits for it before reading its inputs
+  const double *stage_src;
+  double *stage_dst;
+  int stage_len;
 };
 
 // U* = nominal + N / Z, the clipped command and the shifted warm start
@@ -940,7 +946,7 @@ constexpr int kMergeHelpers = 127;
 // merge words after the ticket and the prologue flag: the epoch shares their
 // line (read once per CTA); the polled flag (+ count) and the done counter
 // get lines of their own so the waiting helpers do not contend with them
-constexpr int kHcFlag = 32, kHcCount = 33, kHcDone = 64, kHcWords = 96;
+constexpr int kHcFlag = 32, kHcCount = 33, kHcDone = 64, kHcStage = 80, kHcWords = 96;
 constexpr int kLightMax = 32;  // up to this many nonzero weights the merging CTA computes N alone
 constexpr int kSliceE = 8;     // N elements per slice pass
 // io.max_helpers (host: min(kMergeHelpers, resident CTA slots - 2)) keeps the
@@ -1482,6 +1488,29 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
   return true;
 }
 
+// Session staging (see SmpcIO::stage_src).  The staging word holds
+// epoch + 1 of the launch that filled the device copy; the epoch advances only
+// after the merge, which no CTA of this launch can have passed yet.
+__device__ __forceinline__ void stage_inputs(const SmpcIO &io, int ctas) {
+  unsigned int *hc = io.counters + (ctas + kGroup - 1) / kGroup + 2;
+  if (blockIdx.x == 0) {
+    for (int i = threadIdx.x; i < io.stage_len; i += blockDim.x) io.stage_dst[i] = __ldcv(io.stage_src + i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int ep = *reinterpret_cast<volatile unsigned int *>(hc);
+      fence_acq_rel_gpu();  // cumulative over the CTA's copies (ordered by the barrier)
+      *reinterpret_cast<volatile unsigned int *>(hc + kHcStage) = ep + 1u;
+    }
+  } else {
+    if (threadIdx.x == 0) {
+      const unsigned int want = *reinterpret_cast<volatile unsigned int *>(hc) + 1u;
+      SpinGuard g;
+      while (ld_acquire_gpu(hc + kHcStage) != want) g.pause(20);
+    }
+  }
+  __syncthreads();
+}
+
 // Fused SMPC step: rollout -> CTA partial -> group merge -> global merge
 // [-> U*, clip, shift, re-evaluation].
 template <typename T, typename ET, int MAXJ, typename Topo>
@@ -1491,6 +1520,9 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
   const SmemLayout L = smem_layout(is_dyn_v<Topo> ? P.ns : 0, sizeof(T), kMergeScratch);
   const Shared S = carve(smem_raw, L);
   Dyn<T> &D = *reinterpret_cast<Dyn<T> *>(S.dyn);
+  if constexpr (!is_dyn_v<Topo>) {
+    if (io.stage_src) stage_inputs(io, (int)gridDim.x - 1);
+  }
   if (threadIdx.x < 32) load_dyn<T>(P, io.dyn, D);
   __syncthreads();
   const int64_t cta_m0 = (int64_t)blockIdx.x * smpc_nw<Topo>();
@@ -2112,7 +2144,8 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
                        const double *nominal, int64_t M, int64_t m_offset, int precision, double *costs,
                        uint8_t *flags, double *part_out, double *out, void *workspace, size_t workspace_bytes,
                        cudaStream_t s, const NoiseGen *gen = nullptr, bool counters_zeroed = false,
-                       double *out_host = nullptr) {
+                       double *out_host = nullptr, const double *stage_src = nullptr,
+                       double *stage_dst = nullptr, int64_t stage_len = 0) {
   int rc = prob_checks(prob, precision, dtype);
   if (rc) return rc;
   VPB_REQUIRE(eps && nominal && M >= 1, "bad arguments to the SMPC step");
@@ -2146,6 +2179,9 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   io.dyn = prob->dyn_state;
   io.trace = g_smpc_trace;
   io.out_host = out_host;
+  io.stage_src = stage_src;
+  io.stage_dst = stage_dst;
+  io.stage_len = (int)stage_len;
   const int topo = fixed_topology_disabled() ? 0 : topo_id(prob);
   if (gen) {  // fused draw (eps is the output buffer of the draws)
     io.gen = *gen;
@@ -2253,9 +2289,12 @@ namespace vpb {
 int smpc_generate_session(const vpb_problem *prob, const vpb_field *field, const uint64_t *seed_dev, int64_t window,
                           const double *sigma, const double *nominal, int64_t M, int precision, void *eps_out,
                           double *out, double *out_host, void *workspace, size_t workspace_bytes,
-                          cudaStream_t s) {
+                          cudaStream_t s, const double *stage_src, double *stage_dst, int64_t stage_len) {
   const int64_t n = prob->n_joints;
   const bool fused = precision == VPB_PREC_F32 && window <= 5 && !fixed_topology_disabled() && topo_id(prob) == 1;
+  const bool in_kernel_stage = fused && getenv("VPB_SESSION_COPY_NODE") == nullptr;
+  if (stage_src && !in_kernel_stage)
+    VPB_CUDA(cudaMemcpyAsync(stage_dst, stage_src, (size_t)stage_len * 8, cudaMemcpyHostToDevice, s));
   if (fused) {
     NoiseGen g;
     memset(&g, 0, sizeof(g));
@@ -2263,7 +2302,8 @@ int smpc_generate_session(const vpb_problem *prob, const vpb_field *field, const
     g.window = (int)window;
     for (int64_t j = 0; j < n; ++j) g.sigma[j] = (float)sigma[j];
     return smpc_launch(prob, field, eps_out, VPB_DTYPE_F32, nominal, M, 0, precision, nullptr, nullptr, nullptr, out,
-                       workspace, workspace_bytes, s, &g, true, out_host);
+                       workspace, workspace_bytes, s, &g, true, out_host, in_kernel_stage ? stage_src : nullptr,
+                       stage_dst, stage_len);
   }
   const int dtype = precision == VPB_PREC_F32 ? VPB_DTYPE_F32 : VPB_DTYPE_F64;
   int rc = vpb_sample_perturbations(0, seed_dev, 0, M, prob->horizon, n, window, sigma, dtype, eps_out, s);

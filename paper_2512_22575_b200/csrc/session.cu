@@ -3,9 +3,12 @@
 // Planner.smpc_step (vp/planner.py:594-630) with host buffers in and out: the
 // per-call block (start state, goal, seed, field pointer, warm start) is
 // written to pinned memory, one captured CUDA graph replays
-//   H2D copy of the block -> SMPC step (the perturbations are drawn inside
-//   the fused step kernel for the compiled topology; the kernel's last CTA
-//   writes the packed result straight into pinned host memory),
+//   SMPC step: block 0 of the fused step kernel copies the block from the
+//   host-mapped buffer to the device while the other CTAs wait on a flag (no
+//   copy node: a graph copy node costs ~9 us on B200, the in-kernel copy one
+//   PCIe round trip); the perturbations are drawn inside the kernel for the
+//   compiled topology; the merging CTA writes the packed result straight into
+//   pinned host memory,
 // and the call returns after a stream synchronisation.  The session owns its
 // device buffers (allocated once at creation), so a step does no allocation,
 // no attribute setting and no per-kernel host work.
@@ -51,14 +54,13 @@ void release(vpb_smpc_session *s) {
 
 int enqueue(vpb_smpc_session *s, bool copies) {
   const int64_t nom = s->dyn_len + 2;
-  // (VPB_SESSION_AB: 1 = no H2D node, 2 = no host result, for overhead A/B only)
-  static const int ab = getenv("VPB_SESSION_AB") ? atoi(getenv("VPB_SESSION_AB")) : 0;
-  if (copies && ab != 1)
-    VPB_CUDA(cudaMemcpyAsync(s->d_in, s->h_in, (size_t)s->in_len * 8, cudaMemcpyHostToDevice, s->stream));
+  // the per-call block travels host-mapped -> device inside the fused step
+  // kernel (or by a copy that smpc_generate_session enqueues on other paths);
   // the step kernel writes the result straight into the pinned host buffer
   return vpb::smpc_generate_session(&s->prob, &s->field, reinterpret_cast<const uint64_t *>(s->d_in + s->dyn_len),
                                     s->window, s->sigma, s->d_in + nom, s->M, s->precision, s->eps, s->d_out,
-                                    ab == 2 ? nullptr : s->h_out, s->ws, s->ws_bytes, s->stream);
+                                    s->h_out, s->ws, s->ws_bytes, s->stream, copies ? s->h_in : nullptr, s->d_in,
+                                    s->in_len);
 }
 
 // 3x3 row-major helpers (host, double)

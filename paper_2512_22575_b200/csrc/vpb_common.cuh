@@ -43,10 +43,14 @@ int sm_count();
 
 // Session step (rollout.cu): counters pre-zeroed, result also written to a
 // host-mapped buffer by the kernel (session.cu).
+// The per-call block [stage_src, + stage_len) (host-mapped) reaches its
+// device copy stage_dst either inside the fused kernel (block 0 copies it,
+// the other CTAs wait on a flag: no copy node in the session graph) or, on
+// the other paths, by a copy enqueued first.
 int smpc_generate_session(const vpb_problem *prob, const vpb_field *field, const uint64_t *seed_dev, int64_t window,
                           const double *sigma, const double *nominal, int64_t M, int precision, void *eps_out,
                           double *out, double *out_host, void *workspace, size_t workspace_bytes,
-                          cudaStream_t s);
+                          cudaStream_t s, const double *stage_src, double *stage_dst, int64_t stage_len);
 
 }  // namespace vpb
 
