@@ -32,6 +32,12 @@
 
 namespace vpb {
 
+// The fixed-topology SMPC kernel uses static shared memory so that ptxas may
+// spill registers to shared memory (VPB_NO_SMEM_SPILL: the old dynamic layout)
+#ifndef VPB_NO_SMEM_SPILL
+#define VPB_SMEM_SPILL 1
+#endif
+
 constexpr int NW = 8;                    // candidate warps per CTA (generic path, rollout kernel)
 constexpr int NWF = 4;                   // candidate warps per CTA of the fixed-topology SMPC kernel
 constexpr int kThreads = (NW + 1) * 32;  // + terminal warp
@@ -111,10 +117,10 @@ struct SmemLayout {
   size_t centers, sums, cost, qH, fail, tfail, dyn, pro, misc, scratch, total;
 };
 
-__host__ __device__ inline size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
+__host__ __device__ constexpr size_t al16(size_t v) { return (v + 15) & ~(size_t)15; }
 
-__host__ __device__ inline SmemLayout smem_layout(int ns, size_t tsize, int scratch_doubles) {
-  SmemLayout L;
+__host__ __device__ constexpr SmemLayout smem_layout(int ns, size_t tsize, int scratch_doubles) {
+  SmemLayout L{};
   size_t o = 0;
   L.centers = o;
   o = al16(o + (size_t)NW * (ns > 0 ? ns : 1) * 3 * 32 * tsize);
@@ -1516,7 +1522,22 @@ __device__ __forceinline__ void stage_inputs(const SmpcIO &io, int ctas) {
 template <typename T, typename ET, int MAXJ, typename Topo>
 __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>())
     smpc_kernel(const __grid_constant__ Prob<T> P, const __grid_constant__ SmpcIO io) {
+#ifdef VPB_SMEM_SPILL
+  // the fixed path's layout is a compile-time constant: static shared memory,
+  // and the register spills of the 72-register budget go to shared memory
+  // instead of local memory (which 7 CTAs per SM push out of L1 into L2)
+  unsigned char *smem_raw;
+  if constexpr (!is_dyn_v<Topo>) {
+    asm volatile(".pragma \"enable_smem_spilling\";");
+    __shared__ __align__(16) unsigned char smem_fixed[smem_layout(0, sizeof(T), kMergeScratch).total];
+    smem_raw = smem_fixed;
+  } else {
+    extern __shared__ __align__(16) unsigned char smem_dyn[];
+    smem_raw = smem_dyn;
+  }
+#else
   extern __shared__ __align__(16) unsigned char smem_raw[];
+#endif
   const SmemLayout L = smem_layout(is_dyn_v<Topo> ? P.ns : 0, sizeof(T), kMergeScratch);
   const Shared S = carve(smem_raw, L);
   Dyn<T> &D = *reinterpret_cast<Dyn<T> *>(S.dyn);
@@ -1993,7 +2014,12 @@ static int launch_smpc_t(const Prob<T> &P, const SmpcIO &io, int topo, cudaStrea
     SmpcIO io2 = io;
     const int slots = resident_slots(k, threads, smem);
     io2.max_helpers = slots - 2 < kMergeHelpers ? (slots - 2 > 0 ? slots - 2 : 0) : kMergeHelpers;
-    k<<<(unsigned)ctas, threads, smem, s>>>(P, io2);
+#ifdef VPB_SMEM_SPILL
+    const size_t dsm = topo == 1 ? 0 : smem;
+#else
+    const size_t dsm = smem;
+#endif
+    k<<<(unsigned)ctas, threads, dsm, s>>>(P, io2);
   };
 #ifdef VPB_QUICK
   if constexpr (!std::is_same_v<T, float> || !std::is_same_v<ET, float>) return VPB_ERR_ARG;
