@@ -14,6 +14,7 @@
 // ballot.  Voxels outside the robot's bounding box skip the sphere test;
 // voxels whose projection misses the image touch no memory at all.
 #include <climits>
+#include <cstdlib>
 
 #include "vpb_common.cuh"
 
@@ -48,6 +49,11 @@ struct FusionArgs {
   vpb_journal journal;  // undo records of the modified words (journal.idx == null: off)
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr2[VPB_MAX_MASK_SPHERES];
+  // fp32 mask-sphere classification: centre, and squared radii below which a
+  // voxel centre is certainly inside / above which certainly outside (the
+  // reference's strict fp64 test decides only the thin shell in between)
+  float mcf[VPB_MAX_MASK_SPHERES * 3];
+  float mr2_in[VPB_MAX_MASK_SPHERES], mr2_out[VPB_MAX_MASK_SPHERES];
 };
 
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
@@ -253,10 +259,47 @@ __device__ __forceinline__ void line_intervals(const FusionArgs &A, const Frustu
   }
 }
 
+// Voxels the fp32 prefilter cannot decide take the exact fp64 path.  They are
+// a few per cent of the footprint but scattered: run in place, almost every
+// 32-voxel word would carry one and drag its whole warp through the fp64
+// path.  Instead each warp queues them (x, y, z in shared memory) and runs
+// them 32 at a time, one per lane; a queued voxel's word was journaled when it
+// was queued, and its occupancy bit is set or cleared atomically.
+constexpr int kFuseQueue = 64;  // per warp: a word adds <= 32 entries, a flush takes 32
+
+__device__ __forceinline__ void flush_exact(const FusionArgs &A, int4 *q, int &qn, int lane, bool all) {
+  while (qn >= 32 || (all && qn > 0)) {
+    const int take = qn < 32 ? qn : 32;
+    const int base = qn - take;
+    bool touched = false;
+    double newval = 0.0;
+    int64_t g = 0, x = 0, y = 0, z = 0;
+    if (lane < take) {
+      const int4 e = q[base + lane];
+      x = e.x, y = e.y, z = e.z;
+      g = (x * A.gy + y) * A.gz + z;
+      touched = exact_voxel(A, x, y, z, g, &newval);
+      if (touched) {
+        A.log_odds[g] = newval;
+        A.observed[g] = 1;
+        if (A.occ_bits != nullptr) {
+          uint32_t *ow = A.occ_bits + (x * A.gy + y) * A.words_z + (z >> 5);
+          const uint32_t bit = 1u << (z & 31);
+          if (newval >= A.l_thr) atomicOr(ow, bit);
+          else atomicAnd(ow, ~bit);
+        }
+      }
+    }
+    qn = base;
+    __syncwarp();
+  }
+}
+
 // Persistent: each warp takes (x, y) lines of the footprint; per line the
 // 32-voxel words overlapping its intervals run the per-voxel prefilter.
 __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ FusionArgs A) {
   __shared__ Frustum Fs;
+  __shared__ int4 queue[8][kFuseQueue];
   if (threadIdx.x == 0) frustum_setup(A, Fs);
   __syncthreads();
   const Frustum F = Fs;
@@ -265,6 +308,8 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
   if (nx <= 0 || ny <= 0) return;
   const int64_t lines = (int64_t)nx * ny;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  int4 *q = queue[threadIdx.x >> 5];
+  int qn = 0;  // warp-uniform queue length
   for (int64_t li = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); li < lines; li += warps) {
     const int64_t x = F.xlo + li / ny, y = F.ylo + li % ny;
     Interval ia, im;
@@ -304,8 +349,22 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
       int fast = 0;  // 1 = certain hit, 2 = certain miss (fp32 classification)
       if (in_box) {
         const float pzf = A.of2 + ((float)z + 0.5f) * A.voxf;
+        int mcls = 0;  // robot mask (vp/mapping.py:310-325): 0 outside all, 1 certainly inside one, 2 unsure
         if (line_mask && pzf >= A.bb_lo[2] && pzf <= A.bb_hi[2]) {
-          exact = true;  // possibly inside a mask sphere
+          for (int sm = 0; sm < A.n_mask; ++sm) {
+            const float dx = pxf - A.mcf[3 * sm + 0], dy = pyf - A.mcf[3 * sm + 1], dz = pzf - A.mcf[3 * sm + 2];
+            const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            if (d2 <= A.mr2_in[sm]) {
+              mcls = 1;
+              break;
+            }
+            if (d2 < A.mr2_out[sm]) mcls = 2;
+          }
+        }
+        if (mcls == 1) {
+          fast = 3;  // masked: new value min(old, 0), observed
+        } else if (mcls == 2) {
+          exact = true;  // within fp32 error of a sphere surface
         } else {
           const float qzf = fmaf(A.rf[8], pzf, qz0);
           if (qzf < -dq) {
@@ -358,18 +417,21 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
       bool touched = false;
       double newval = 0.0;
       const int64_t g = gline + z;
-      if (fast) {
+      if (fast == 3) {
+        const double old = A.log_odds[g];
+        newval = old > 0.0 ? 0.0 : old;
+        touched = true;
+      } else if (fast) {
         // certain hit / miss: the reference's fp64 update, bit for bit
         double value = dadd(A.log_odds[g], fast == 1 ? A.l_hit : A.l_miss);
         if (value < A.l_min) value = A.l_min;
         else if (value > A.l_max) value = A.l_max;
         newval = value;
         touched = true;
-      } else if (exact) {
-        touched = exact_voxel(A, x, y, z, g, &newval);
       }
       const unsigned touched_mask = __ballot_sync(kFull, touched);
-      if (touched_mask == 0u) continue;
+      const unsigned exact_mask = __ballot_sync(kFull, exact);
+      if ((touched_mask | exact_mask) == 0u) continue;
       uint32_t *ow = A.occ_bits != nullptr ? A.occ_bits + (x * A.gy + y) * A.words_z + wz : nullptr;
       if (A.journal.idx != nullptr) {
         // undo record of this word before its first write (snapshot journal):
@@ -394,12 +456,21 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
         A.log_odds[g] = newval;
         A.observed[g] = 1;
       }
-      if (ow != nullptr) {
+      if (ow != nullptr && touched_mask != 0u) {
         const unsigned occ_mask = __ballot_sync(kFull, touched && newval >= A.l_thr);
         if (lane == 0) *ow = (*ow & ~touched_mask) | (occ_mask & touched_mask);
       }
+      if (exact_mask != 0u) {
+        __syncwarp();  // (the word's plain occupancy update above precedes the queued voxels' atomics)
+        if (exact) q[qn + __popc(exact_mask & ((1u << lane) - 1u))] = make_int4((int)x, (int)y, (int)z, 0);
+        qn += __popc(exact_mask);
+        __syncwarp();
+        flush_exact(A, q, qn, lane, false);
+      }
     }
   }
+  __syncwarp();
+  flush_exact(A, q, qn, lane, true);
 }
 
 struct MaskPixArgs {
@@ -627,6 +698,33 @@ static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
   int rc = fill_mask(centers, radii, n_mask, A.mc, A.aabb_lo, A.aabb_hi);
   if (rc) return rc;
   for (int64_t s = 0; s < n_mask; ++s) A.mr2[s] = radii[s] * radii[s];
+  {
+    // fp32 sphere test bounds.  A voxel centre's fp32 coordinates are off by
+    // <= 2^-23 (|origin| + |(i + 1/2) voxel|) per rounding (two roundings), a
+    // centre's by 2^-24 |c|; dx = p_f - c_f adds one more rounding.  delta
+    // bounds |dx_f - dx| per axis (4x margin); the squared distance then
+    // carries <= 2 sqrt(3) delta d + 3 delta^2 from the coordinates and
+    // < 1e-6 d^2 from its own three roundings.
+    double cmax = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const double o = k == 0 ? grid->origin[0] : (k == 1 ? grid->origin[1] : grid->origin[2]);
+      const double far = fabs(o) + (double)(grid->dims[k] + 1) * grid->voxel;
+      cmax = fmax(cmax, far);
+    }
+    for (int64_t s = 0; s < n_mask; ++s)
+      for (int k = 0; k < 3; ++k) cmax = fmax(cmax, fabs(centers[3 * s + k]) + fabs(radii[s]));
+    const double delta = 4.0 * (3.0 * 1.2e-7 * cmax) + 1e-12;
+    for (int64_t s = 0; s < n_mask; ++s) {
+      for (int k = 0; k < 3; ++k) A.mcf[3 * s + k] = (float)centers[3 * s + k];
+      const double r = fabs(radii[s]);
+      const double err = 2.0 * 1.7320508075688772 * delta * (r + 4.0 * delta) + 3.0 * delta * delta;
+      const double in2 = r * r * (1.0 - 4e-6) - err;
+      const double out2 = r * r * (1.0 + 4e-6) + err;
+      // rounded towards the safe side
+      A.mr2_in[s] = in2 > 0.0 ? nextafterf((float)in2, 0.0f) : -1.0f;
+      A.mr2_out[s] = nextafterf((float)out2, 3.0e38f);
+    }
+  }
   A.log_odds = grid->log_odds;
   A.observed = grid->observed;
   A.occ_bits = grid->occ_bits;
@@ -698,9 +796,17 @@ static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
       A.mask_i_hi[k] = 0;
     }
   }
-  // persistent: warps stride over the footprint lines each CTA derives
+  // persistent: warps stride over the footprint lines each CTA derives; one
+  // resident wave (every CTA pays the frustum setup once)
+  static int occ = 0;
+  if (occ == 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fuse_kernel, 256, 0) != cudaSuccess) {
+    cudaGetLastError();
+    occ = 4;
+  }
   const int64_t max_ctas = ceil_div(A.n0 * A.n1, 8);
-  const int64_t ctas = max_ctas < (int64_t)sm_count() * 8 ? max_ctas : (int64_t)sm_count() * 8;
+  static const int per_sm_env = getenv("VPB_FUSE_CTAS_PER_SM") ? atoi(getenv("VPB_FUSE_CTAS_PER_SM")) : 0;
+  const int64_t slots = (int64_t)sm_count() * (per_sm_env > 0 ? per_sm_env : (occ > 0 ? occ : 4));
+  const int64_t ctas = max_ctas < slots ? max_ctas : slots;
   fuse_kernel<<<(unsigned)ctas, 256, 0, as_stream(stream)>>>(A);
   return check_launch("fuse_kernel");
 }
