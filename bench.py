@@ -676,12 +676,88 @@ def cpu_baseline(args, S):
     return out
 
 
+def _import_reference():
+    """The unmodified reference (voxplan, Python + numba) from baseline/_ref
+    (pip --target install), or None."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "voxplan").is_dir():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import voxplan  # noqa: F401
+        from voxplan import config as vconfig, mapping as vmapping, parallel as vparallel, planner as vplanner
+        from voxplan import robot as vrobot
+    except Exception as exc:  # pragma: no cover - depends on the box
+        print(f"reference not importable ({exc}); timing the oracle port instead", file=sys.stderr)
+        return None
+    return vconfig, vmapping, vparallel, vplanner, vrobot
+
+
+def run_reference_stock(args, mods) -> bool:
+    """--impl reference through the reference's own public API and stock code
+    path: voxplan.planner.Planner.smpc_step (numba, all host threads) on the C3
+    workload, the field from voxplan.mapping.edt_3d of the C2 bench map (whose
+    log-odds the host oracle fuses: bitwise the reference's fusion, pinned by
+    tests/test_oracle_golden.py), the warm start fed back every step as the
+    reference's own CLI bench and closed loop do (vp/cli.py:286-292,
+    vp/sim.py:484-488)."""
+    vconfig, vmapping, vparallel, vplanner, vrobot = mods
+    from oracle import scene as osc
+
+    m = args.samples * max(1, args.gpus)
+    scene_map = osc.bench_map(args.grid)  # host fusion x2 of the C2 scene (input data, untimed)
+    grid = vmapping.VoxelGrid(scene_map["origin"], scene_map["voxel"], (args.grid,) * 3)
+    grid.log_odds[...] = scene_map["log_odds"]
+    field = vmapping.edt_3d(grid, outside_default=0.8)
+    chain, model = vrobot.load_robot(vconfig.bundled_scenario_path("robot_7dof"))
+    params = vconfig.planner_params(chain.dof, {"samples": m, "horizon": args.horizon})
+    planner = vplanner.Planner(chain, model, params)
+    state = vrobot.JointState.resting(np.full(7, 0.05))
+    goal = vrobot.forward_kinematics(chain, np.full(7, 0.35))[-1]
+    threads = vparallel.set_threads(os.cpu_count() or 1)
+    nominal = None
+    for k in range(max(1, args.warmup)):  # the first call JIT-compiles the numba kernels
+        nominal = planner.smpc_step(state, goal, field, nominal, k).next_nominal
+    times = []
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        nominal = planner.smpc_step(state, goal, field, nominal, 1000 + k).next_nominal
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    value = m / t
+    wl = "C3" if (args.samples, args.horizon) == (4096, 32) else "custom"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (CLI bench scene 256^3 + 7-DoF body mask fused on the host; the reference's own edt_3d "
+                "and Planner.smpc_step)",
+        "config": {"workload": f"{wl}: SMPC iteration M={args.samples}/rank x H={args.horizon}, 7-DoF robot_7dof, "
+                               f"field = C2 {args.grid}^3 masked map",
+                   "samples_per_rank": args.samples, "horizon": args.horizon, "grid": [args.grid] * 3,
+                   "total_samples": m},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} full smpc_step iterations of M={m} through the unmodified "
+                                   f"reference (baseline/_ref, numba parallel on {threads} threads), warm start "
+                                   f"fed back, after {max(1, args.warmup)} warm-up steps (JIT)",
+                         "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "product_modules_loaded": sorted(k for k in sys.modules if k.startswith("paper_2512_22575_b200")),
+    }
+    print(json.dumps(line), flush=True)
+    return True
+
+
 def run_reference(args):
     """--impl reference: the reference's path restated on the host cores
     (oracle/: C fp64 restatement + the reference's numpy sampler), on the
     same workload as our arm.  Imports nothing from the product package."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return
+    mods = None if os.environ.get("VPB_REFERENCE_PORT") else _import_reference()
+    if mods is not None and run_reference_stock(args, mods):
         return
     import oracle
     from oracle import scene as osc
