@@ -127,6 +127,11 @@ typedef struct {
   unsigned long long *count; /* records written (dev) */
   unsigned int *overflow;    /* set if a record did not fit (dev) */
   uint64_t capacity;
+  /* segment bookkeeping, done on the device before the update's first record:
+   * if reset != 0, count = 0; then starts[seg] = count (starts may be NULL) */
+  int64_t *starts;
+  int32_t seg;
+  int32_t reset;
 } vpb_journal;
 
 /* vpb_update_occupancy that also journals the words it modifies

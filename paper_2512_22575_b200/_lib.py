@@ -55,7 +55,7 @@ class VpbGrid(ctypes.Structure):
 
 class VpbJournal(ctypes.Structure):
     _fields_ = [("idx", _p), ("lo", _p), ("ob", _p), ("occ", _p), ("count", _p), ("overflow", _p),
-                ("capacity", ctypes.c_uint64)]
+                ("capacity", ctypes.c_uint64), ("starts", _p), ("seg", _i32), ("reset", _i32)]
 
 
 class VpbField(ctypes.Structure):

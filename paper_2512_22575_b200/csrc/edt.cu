@@ -947,20 +947,37 @@ static int edt_tiled(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
   const size_t smem_x = x_tile_rows(n[0]) * 32 * 4 + sizeof(SegLine<KS>) * 32 + 16;
   auto kzy = edt_zy_kernel<WIDE, KS>;
   auto kx = edt_x_kernel<WIDE, KS>;
-  VPB_CUDA(cudaFuncSetAttribute(kzy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
-  VPB_CUDA(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
-  CUtensorMap gmap;
-  int rc = make_g_map(&gmap, g2, n[0], n[1], n[2]);
-  if (rc) return rc;
+  // host-side setup cached per (device, shape, g buffer): attributes, the
+  // tensor map and the occupancy queries cost ~10 us of host time per call
+  struct Setup {
+    int dev = -1;
+    int64_t n0 = 0, n1 = 0, n2 = 0;
+    const int32_t *g = nullptr;
+    CUtensorMap gmap;
+    int occ_zy = 0, occ_x = 0;
+  };
+  static thread_local Setup cache;
+  int dev = 0;
+  VPB_CUDA(cudaGetDevice(&dev));
+  int rc = VPB_OK;
+  if (cache.dev != dev || cache.n0 != n[0] || cache.n1 != n[1] || cache.n2 != n[2] || cache.g != g2) {
+    VPB_CUDA(cudaFuncSetAttribute(kzy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_zy));
+    VPB_CUDA(cudaFuncSetAttribute(kx, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_x));
+    if ((rc = make_g_map(&cache.gmap, g2, n[0], n[1], n[2]))) return rc;
+    VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache.occ_zy, kzy, 32 * KS, smem_zy));
+    VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cache.occ_x, kx, 32 * KS, smem_x));
+    cache.dev = dev;
+    cache.n0 = n[0], cache.n1 = n[1], cache.n2 = n[2];
+    cache.g = g2;
+  }
+  const CUtensorMap gmap = cache.gmap;
   const int zch = (int)((n[2] + 31) / 32);
   static const double l2_mb = getenv("VPB_EDT_L2_MB") ? atof(getenv("VPB_EDT_L2_MB")) : 128.0;
   const double chunk_mb = (double)n[0] * (double)n[1] * 32.0 * 4.0 / 1048576.0;
   int group = (int)(l2_mb / chunk_mb);
   group = group < 1 ? 1 : (group > zch ? zch : group);
   // persistent grids: every SM filled with as many CTAs as smem / registers allow
-  int occ_zy = 0, occ_x = 0;
-  VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_zy, kzy, 32 * KS, smem_zy));
-  VPB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_x, kx, 32 * KS, smem_x));
+  const int occ_zy = cache.occ_zy, occ_x = cache.occ_x;
   const int64_t slots_zy = (int64_t)sm_count() * (occ_zy > 0 ? occ_zy : 1);
   const int64_t slots_x = (int64_t)sm_count() * (occ_x > 0 ? occ_x : 1);
   for (int z0 = 0; z0 < zch; z0 += group) {

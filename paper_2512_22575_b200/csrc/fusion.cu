@@ -484,6 +484,10 @@ struct MaskPixArgs {
   int *bbox;          // optional: [umin, umax, vmin, vmax] of usable pixels
   int *partials;      // per-CTA rectangles (bbox != null)
   unsigned *counter;  // CTA ticket, zero between launches (the last CTA resets it)
+  // journal segment bookkeeping (vpb_journal.starts / seg / reset), before fusion's first record
+  unsigned long long *j_count;
+  int64_t *j_starts;
+  int j_seg, j_reset;
   double pad;
   double mc[VPB_MAX_MASK_SPHERES * 3];
   double mr[VPB_MAX_MASK_SPHERES];
@@ -491,6 +495,10 @@ struct MaskPixArgs {
 
 // vp/mapping.py:357-380, one thread per pixel.
 __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constant__ MaskPixArgs A) {
+  if (A.j_count != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (A.j_reset) *A.j_count = 0ull;
+    if (A.j_starts != nullptr) A.j_starts[A.j_seg] = (int64_t)*A.j_count;
+  }
   const int64_t idx0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool px = idx0 < A.width * A.height;  // (threads past the image join the CTA reduction)
   const int64_t idx = px ? idx0 : 0;
@@ -655,7 +663,7 @@ int vpb_occ_bits_from_log_odds(const vpb_grid *grid, double thr, void *stream) {
 
 static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const double *centers,
                               const double *radii, int64_t n_mask, double pad, uint8_t *out, int encode,
-                              int *bbox, void *stream) {
+                              int *bbox, void *stream, const vpb_journal *journal = nullptr) {
   VPB_REQUIRE(depth && cam && out, "null argument to vpb_masked_pixels");
   MaskPixArgs A;
   memset(&A, 0, sizeof(A));
@@ -679,8 +687,21 @@ static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const 
     A.partials = bbox + 8;
   }
   A.pad = pad;
+  if (journal != nullptr && journal->count != nullptr) {
+    A.j_count = journal->count;
+    A.j_starts = journal->starts;
+    A.j_seg = journal->seg;
+    A.j_reset = journal->reset;
+  }
   const int64_t npx = cam->width * cam->height;
-  if (npx == 0) return VPB_OK;
+  if (npx == 0) {
+    if (A.j_count != nullptr) {  // (no launch to carry the journal bookkeeping)
+      cudaStream_t st = as_stream(stream);
+      if (A.j_reset) VPB_CUDA(cudaMemsetAsync(A.j_count, 0, sizeof(unsigned long long), st));
+      if (A.j_starts) VPB_CUDA(cudaMemcpyAsync(A.j_starts + A.j_seg, A.j_count, 8, cudaMemcpyDeviceToDevice, st));
+    }
+    return VPB_OK;
+  }
   masked_pixels_kernel<<<(unsigned)ceil_div(npx, 256), 256, 0, as_stream(stream)>>>(A);
   return check_launch("masked_pixels_kernel");
 }
@@ -844,7 +865,7 @@ int vpb_update_occupancy_journaled(const vpb_grid *grid, const int64_t lo[3], co
   // return; followed by the bounding rectangle of the usable pixels
   const int64_t npx = cam->width * cam->height;
   int *bbox = reinterpret_cast<int *>(pixel_scratch + align_up((size_t)npx, 16));
-  int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, bbox, stream);
+  int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, bbox, stream, journal);
   if (rc) return rc;
   return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, bbox, stream, journal);
 }

@@ -156,7 +156,10 @@ class VoxelGrid:
         return self.params.tau_factor * self.voxel_size
 
     def full_box(self) -> VoxelBox:
-        return VoxelBox((0, 0, 0), self.dims)
+        fb = self.__dict__.get("_full_box")
+        if fb is None:  # (VoxelBox is frozen: one shared instance caches its native views)
+            fb = self.__dict__["_full_box"] = VoxelBox((0, 0, 0), self.dims)
+        return fb
 
     def voxel_center(self, index) -> np.ndarray:
         return self.origin + (np.asarray(index, dtype=float) + 0.5) * self.voxel_size
@@ -268,10 +271,13 @@ class _Journal:
         self.starts = torch.zeros(self.MAX_SEG, dtype=torch.int64, device=self.dev)
         self.idx = self.lo = self.ob = self.occ = None
         self._struct = None
+        self._pending_reset = False
 
     def reset(self) -> None:
+        # the record count is zeroed on the device by the next journaled
+        # update itself (vpb_journal.reset), not by a launch of its own
         if self.nseg or self.bound:
-            self.count.zero_()
+            self._pending_reset = True
         self.nseg = 0
         self.bound = 0
 
@@ -289,15 +295,24 @@ class _Journal:
         j = VpbJournal()
         j.idx, j.lo, j.ob, j.occ = (D.ptr(t) for t in new)
         j.count, j.overflow, j.capacity = D.ptr(self.count), D.ptr(self.overflow), cap
+        j.starts = D.ptr(self.starts)
         self._struct = j
 
     def begin_segment(self, words: int) -> VpbJournal:
         if self.bound + words > self.cap:
+            if self._pending_reset:  # (_grow keeps the first `bound` records, none after a reset)
+                self.count.zero_()
+                self._pending_reset = False
             self._grow(max(2 * self.cap, self.bound + words))
-        self.starts[self.nseg:self.nseg + 1].copy_(self.count)  # device-side: no sync
+        # starts[nseg] = count (after the pending reset, if any), on the device
+        # at the start of the update (vpb_journal.seg / reset)
+        j = self._struct
+        j.seg = self.nseg
+        j.reset = 1 if self._pending_reset else 0
+        self._pending_reset = False
         self.nseg += 1
         self.bound += words
-        return self._struct
+        return j
 
     def restore_into(self, grid: "SnapshotGrid", first_seg: int) -> None:
         """Write the undo records of segments nseg-1 .. first_seg (newest first) into grid."""
@@ -449,8 +464,35 @@ class DepthImage:
     def device_tensor(self, dev: torch.device) -> torch.Tensor:
         if self._dev is None or self._dev.device != dev:
             src = self._host if self._host is not None else self._dev.cpu().numpy()
-            self._dev = torch.from_numpy(np.ascontiguousarray(src)).to(dev, non_blocking=False)
+            self._dev = _upload_depth(np.ascontiguousarray(src), dev)
         return self._dev
+
+
+# Depth frames reach the device through two pinned staging buffers per shape
+# (ping-pong, each guarded by the event of its last copy): the H2D copy is
+# asynchronous on the current stream instead of a pageable, host-blocking one.
+_PINNED: dict = {}
+
+
+def _upload_depth(src: np.ndarray, dev: torch.device) -> torch.Tensor:
+    key = (src.shape, dev)
+    slots = _PINNED.get(key)
+    if slots is None:
+        slots = _PINNED[key] = [[torch.empty(src.shape, dtype=torch.float64, pin_memory=True), None]
+                                for _ in range(2)]
+    slot = slots.pop(0)
+    slots.append(slot)
+    pin, ev = slot
+    if ev is not None:
+        ev.synchronize()  # the copy that last read this buffer is done
+    np.copyto(pin.numpy(), src)
+    out = torch.empty(src.shape, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    out.copy_(pin, non_blocking=True)
+    if ev is None:
+        ev = slot[1] = torch.cuda.Event()
+    ev.record(stream)
+    return out
 
 
 def _mask_arrays(mask):
@@ -564,13 +606,16 @@ def edt_3d(grid: VoxelGrid, volume: VoxelBox | None = None, outside_default: flo
     ``pass_order`` (validated for API parity)."""
     box = volume or grid.full_box()
     grid.validate_box(box)
-    if sorted(pass_order) != ["x", "y", "z"]:
+    if pass_order != ("y", "x", "z") and sorted(pass_order) != ["x", "y", "z"]:
         raise ValueError(f"pass_order must permute x, y, z; got {pass_order}")
     grid._ensure_bits()
     dev = grid.device
     blo, n = box.native()
     L = load()
-    ws_bytes = int(L.vpb_edt3d_workspace_bytes(n))
+    ws_bytes = box.__dict__.get("_edt_ws_bytes")
+    if ws_bytes is None:
+        ws_bytes = int(L.vpb_edt3d_workspace_bytes(n))
+        object.__setattr__(box, "_edt_ws_bytes", ws_bytes)
     ws = D.Workspace.get(dev, "edt", ws_bytes)
     out = torch.empty(box.shape, dtype=torch.float32, device=dev)
     check(L.vpb_edt3d(grid._struct(), blo, n, grid.params.l_occ_threshold, 1, D.ptr(out),
