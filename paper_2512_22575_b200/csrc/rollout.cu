@@ -1511,7 +1511,10 @@ __device__ __forceinline__ void stage_inputs(const SmpcIO &io, int ctas) {
     if (threadIdx.x == 0) {
       const unsigned int want = *reinterpret_cast<volatile unsigned int *>(hc) + 1u;
       SpinGuard g;
-      while (ld_acquire_gpu(hc + kHcStage) != want) g.pause(20);
+#ifndef VPB_STAGE_SLEEP_NS
+#define VPB_STAGE_SLEEP_NS 20
+#endif
+      while (ld_acquire_gpu(hc + kHcStage) != want) g.pause(VPB_STAGE_SLEEP_NS);
     }
   }
   __syncthreads();
