@@ -830,6 +830,7 @@ struct SmpcIO {
   double *out_host;  // optional host-mapped copy of `out` (+ 1 slot: the done flag), written by the last CTA
   double *cand_terms;  // [M][6] per-candidate sums (fixed path): the re-evaluation shortcut
   int max_helpers;     // helper CTAs of the heavy merge (residency-capped, see merge_helpers)
+  double *hparts;      // heavy merge: per-participant [Z, nonzero count, N (H n)] partials
   // session staging (fixed path): block 0 copies the host-mapped per-call
   // block into its device copy and raises the staging word; every other CTA
   // waits for it before reading its inputs
@@ -937,15 +938,15 @@ __device__ __forceinline__ void fixed_shard_fixup(const Shared &S, int64_t M, do
   }
 }
 
-// exp() out of line: the large-list expansion unrolls its loads, not this
-__device__ __noinline__ double exp_noinline(double x) { return exp(x); }
 
 // Many nonzero weights (a converged planner: costs within ~746 lam of the
-// minimum) make N = sum_k w_k eps_k an (ncand x H n) reduction -- too much
-// for the merging CTA alone.  The CTAs that took the last kMergeHelpers
-// tickets stay resident, spin on a per-launch flag and, when the merge asks
-// for help, each computes a fixed slice of the N elements over all nonzero
-// candidates (fixed order: deterministic).  Words after the ticket
+// minimum) make the weights (one f64 exp each) and N = sum_k w_k eps_k an
+// (ncand x H n) reduction -- too much for the merging CTA alone.  The CTAs
+// that took the last kMergeHelpers tickets stay resident, spin on a
+// per-launch flag and, when the merge asks for help, each takes a contiguous
+// slice of the nonzero-CTA list: its candidates' weights, their Z and their
+// N over all elements (heavy_part); the merger adds the partials in
+// participant order (deterministic).  Words after the ticket
 // (io.counters + groups + 2): epoch, flag = epoch << 2 | state, ncand, done;
 // the epoch advances once per launch, so nothing has to be reset.
 constexpr int kMergeHelpers = 127;
@@ -953,8 +954,11 @@ constexpr int kMergeHelpers = 127;
 // line (read once per CTA); the polled flag (+ count) and the done counter
 // get lines of their own so the waiting helpers do not contend with them
 constexpr int kHcFlag = 32, kHcCount = 33, kHcDone = 64, kHcStage = 80, kHcWords = 96;
+// heavy-merge parameters published with the verdict (on the flag's line):
+// the minimum (f64 bits), the per-warp CTA-list lengths, their stride, the
+// merger's warp count, the CTA-list length
+constexpr int kHcM0 = 34, kHcWcount = 36, kHcSpan = 52, kHcNw = 53, kHcList = 54, kHcParts = 55;
 constexpr int kLightMax = 32;  // up to this many nonzero weights the merging CTA computes N alone
-constexpr int kSliceE = 8;     // N elements per slice pass
 // io.max_helpers (host: min(kMergeHelpers, resident CTA slots - 2)) keeps the
 // spinning helpers from filling every slot while CTAs without a ticket still
 // wait to be scheduled (small MIG / MPS partitions); 0 = the merger alone
@@ -962,63 +966,123 @@ __device__ __forceinline__ int merge_helpers(const SmpcIO &io, int ctas) {
   return ctas - 1 < io.max_helpers ? ctas - 1 : io.max_helpers;
 }
 
-// N elements of participant `part` of `P` (a contiguous slice), over all
-// ncand candidates (lists in global memory), by every thread of the CTA.
-template <typename ET>
-__device__ void n_slice(const SmpcIO &io, const Shared &S, const int *mlist, const double *wlist, int ncand, int hn,
-                        int part, int P, double *dst) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+// Heavy merge, one participant (a helper CTA or the merger): the weights of
+// the candidates of its contiguous slice of the nonzero-CTA list (written to
+// the candidate lists in list order), their Z and nonzero count (summed in
+// list order) and their N = sum w eps over all H n elements (each thread its
+// elements, candidates in list order) -> hparts[part].  The merger then adds
+// the participants' partials in participant order: deterministic.
+template <typename ET, int NWC>
+__device__ void heavy_part(const SmpcIO &io, const Shared &S, const unsigned int *hc, int part, int P, int hn) {
+  const int tid = threadIdx.x, nt = blockDim.x;
   const ET *eps = reinterpret_cast<const ET *>(io.eps);
-  const int per = (hn + P - 1) / P;
-  const int b0 = part * per, b1 = min(hn, b0 + per);
-  // [nw][kSliceE] over the merge's CTA-list slots (kFmCL.., free once the
-  // list is expanded); the record head at kFmRec stays intact
-  double *red = S.scratch + 48;
-#pragma unroll 1
-  for (int e0 = b0; e0 < b1; e0 += kSliceE) {
-    const int E = min(kSliceE, b1 - e0);
-    double acc[kSliceE];
+  const double *costs = io.costs ? io.costs : io.cand_costs;
+  double *wlist = io.group_parts;
+  int *mlist = reinterpret_cast<int *>(io.group_parts + io.M + 64);
+  const int *clist = reinterpret_cast<const int *>(io.group_parts + io.M + 64) + io.M + 64;
+  const unsigned long long m0b = (unsigned long long)__ldcg(hc + kHcM0) | ((unsigned long long)__ldcg(hc + kHcM0 + 1) << 32);
+  const double m0 = __longlong_as_double((long long)m0b);
+  const double inv_lam = 1.0 / io.lam;
+  const int span = (int)__ldcg(hc + kHcSpan), nw = (int)__ldcg(hc + kHcNw), list = (int)__ldcg(hc + kHcList);
+  int wc[16];
 #pragma unroll
-    for (int j = 0; j < kSliceE; ++j) acc[j] = 0.0;
-    // 8 candidates per round trip: indices and weights first, then the gathers
-    // (each thread keeps its candidates k = tid + i nt in increasing order)
-#pragma unroll 1
-    for (int k0 = tid; k0 < ncand; k0 += 8 * nt) {
-      int m[8];
-      double w[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int k = k0 + u * nt;
-        m[u] = k < ncand ? __ldcg(mlist + k) : 0;
-        w[u] = k < ncand ? __ldcg(wlist + k) : 0.0;
+  for (int w = 0; w < 16; ++w) wc[w] = w < nw ? (int)__ldcg(hc + kHcWcount + w) : 0;
+  const int per = (list + P - 1) / P;
+  const int j0 = part * per, j1 = min(list, j0 + per);
+  constexpr int kE = 2;  // N elements per thread and pass (passes over blocks of kE nt elements)
+  double z = 0.0, nzc = 0.0;
+  // [nt] weights and rows of the chunk, in the sphere-centre area (free after
+  // the evaluation; the merge scratch still holds the record head)
+  double *wbuf = reinterpret_cast<double *>(S.centers);
+  int *mbuf = reinterpret_cast<int *>(wbuf + nt);
+  for (int k0 = NWC * j0; k0 < NWC * j1; k0 += nt) {
+    const int k = k0 + tid;
+    double wt = 0.0;
+    int mm = 0;
+    if (k < NWC * j1) {
+      const int j = k / NWC, r = k % NWC;
+      int seg = 0, base = 0;
+      while (seg < nw - 1 && j >= base + wc[seg]) {
+        base += wc[seg];
+        ++seg;
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        if (w[u] == 0.0) continue;  // zero weights (uncompacted list, padding) add exactly nothing
-        const ET *row = eps + (size_t)m[u] * hn + e0;
-#pragma unroll
-        for (int j = 0; j < kSliceE; ++j)
-          if (j < E) acc[j] += w[u] * load_e<ET>(row + j);
+      const int ci = __ldcg(clist + seg * span + (j - base));
+      const int m = ci * NWC + r;
+      if (m < io.M) {
+        const double c = __ldcg(costs + m);
+        wt = c < dinf() ? exp(-(c - m0) * inv_lam) : 0.0;
+        mm = m;
       }
+      mlist[k] = mm;  // (padding slot of the last CTA: weight 0, any valid row)
+      wlist[k] = wt;
     }
-#pragma unroll
-    for (int j = 0; j < kSliceE; ++j) {
-      const double v = warp_sum_d(acc[j]);
-      if (lane == 0) red[warp * kSliceE + j] = v;
+    wbuf[tid] = wt;
+    mbuf[tid] = mm;
+    // Z and the count of the chunk: fixed-shape block reduction (warp xor
+    // trees, then the warps in order), added to the running sums by thread 0
+    const double zw = warp_sum_d(wt), cw = warp_sum_d(wt != 0.0 ? 1.0 : 0.0);
+    double *wred = reinterpret_cast<double *>(mbuf + nt);  // [2][nw]
+    if ((tid & 31) == 0) {
+      wred[tid >> 5] = zw;
+      wred[(nt >> 5) + (tid >> 5)] = cw;
     }
     __syncthreads();
-    if (tid < E) {
-      double v = 0.0;
-      for (int w = 0; w < nw; ++w) v += red[w * kSliceE + tid];
-      dst[e0 + tid] = v;
+    const int cnt = min(nt, NWC * j1 - k0);
+    if (tid == 0) {
+      for (int w = 0; w < (nt >> 5); ++w) {
+        z += wred[w];
+        nzc += wred[(nt >> 5) + w];
+      }
+    }
+    // N: element blocks of kE nt; candidates in groups of kG with every row
+    // load of the group in flight before the in-order accumulation (a zero
+    // weight adds exactly 0); the block's partial sums go to hparts
+    constexpr int kG = 8;
+    double *dstn = io.hparts + (size_t)part * (2 + hn) + 2;
+    for (int eb = 0; eb < hn; eb += kE * nt) {
+      double nacc[kE];
+#pragma unroll
+      for (int q = 0; q < kE; ++q) nacc[q] = k0 == NWC * j0 ? 0.0 : dstn[eb + tid + q * nt < hn ? eb + tid + q * nt : 0];
+      for (int i0 = 0; i0 < cnt; i0 += kG) {
+        double wi[kG];
+        double v[kG][kE];
+#pragma unroll
+        for (int g = 0; g < kG; ++g) {
+          const int i = i0 + g;
+          wi[g] = i < cnt ? wbuf[i] : 0.0;
+          const ET *row = eps + (size_t)(i < cnt ? mbuf[i] : 0) * hn;
+#pragma unroll
+          for (int q = 0; q < kE; ++q) {
+            const int e = eb + tid + q * nt;
+            v[g][q] = (e < hn && wi[g] != 0.0) ? load_e<ET>(row + e) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < kG; ++g)
+#pragma unroll
+          for (int q = 0; q < kE; ++q) nacc[q] += wi[g] * v[g][q];
+      }
+#pragma unroll
+      for (int q = 0; q < kE; ++q) {
+        const int e = eb + tid + q * nt;
+        if (e < hn) dstn[e] = nacc[q];
+      }
     }
     __syncthreads();
+  }
+  double *dst = io.hparts + (size_t)part * (2 + hn);
+  if (tid == 0) {
+    dst[0] = z;
+    dst[1] = nzc;
+  }
+  if (j1 <= j0) {  // empty slice: zero N
+    for (int e = tid; e < hn; e += nt) dst[2 + e] = 0.0;
   }
 }
 
 // A helper CTA (one of the last kMergeHelpers finishers): wait for the merge's
 // verdict; on "help", compute slice `part` and report done.
-template <typename ET>
+template <typename ET, int NWC>
 __device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn, int part, unsigned int ep) {
   unsigned int *c = io.counters + (ctas + kGroup - 1) / kGroup + 2;
   unsigned int *st = reinterpret_cast<unsigned int *>(S.misc + 47);
@@ -1031,10 +1095,10 @@ __device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn
   }
   __syncthreads();
   if (st[0] != 2u) return;
-  const int ncand = (int)st[1];
-  double *gp = io.group_parts;
-  n_slice<ET>(io, S, reinterpret_cast<const int *>(gp + io.M + 64), gp, ncand, hn, part, merge_helpers(io, ctas) + 1,
-              io.rank_part + kPartHead);
+  const int P = (int)__ldcg(c + kHcParts);  // participants: helpers 0 .. P-2 and the merger
+  if (part >= P - 1) return;
+  heavy_part<ET, NWC>(io, S, c, part, P, hn);
+  __syncthreads();
   if (threadIdx.x == 0) {
     fence_acq_rel_gpu();
     atomicAdd(c + kHcDone, 1u);
@@ -1052,8 +1116,6 @@ constexpr int kFmBest = 44;        // local index of the minimum's candidate
 constexpr int kFmCL = 48;          // ints: [nw][kFmCap] nonzero CTAs per warp
 constexpr int kFmML = 120;         // ints: [32] indices of the first nonzero candidates
 constexpr int kFmWN = 136;         // ints: [nw] nonzero CTA count per warp
-// (48..120 again, after the expansion: [nw][kSliceE] N slice reduction, n_slice)
-// smem per CTA must stay under 48 KB / 7 so that 7 CTAs fit the default carveout
 constexpr int kFmCap = 16;
 
 // Final merge of the single-device step, by the last CTA.  Inputs: the CTA
@@ -1260,51 +1322,14 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
       z = wt;
       nz = wt != 0.0 ? 1 : 0;
     }
-  } else {
-    constexpr int B = 8;
-    int seg = 0, base = 0;  // list segment (warp slice of clist) of entry k; k only grows
-#pragma unroll 1
-    for (int k0 = tid; k0 < total; k0 += B * nt) {
-      int m[B];
-#pragma unroll
-      for (int u = 0; u < B; ++u) {  // B independent clist loads
-        const int k = k0 + u * nt;
-        m[u] = -1;
-        if (k < total) {
-          while (seg < nw - 1 && k >= base + wcount[seg] * NWC) {
-            base += wcount[seg] * NWC;
-            ++seg;
-          }
-          const int r = k - base;
-          const int ci = small ? sclist[seg * kFmCap + r / NWC] : clist[seg * span + r / NWC];
-          m[u] = ci * NWC + (r % NWC);
-        }
-      }
-      double c[B];
-#pragma unroll
-      for (int u = 0; u < B; ++u) c[u] = (m[u] >= 0 && m[u] < io.M) ? costs[m[u]] : dinf();  // B independent loads
-#pragma unroll
-      for (int u = 0; u < B; ++u) {
-        const int k = k0 + u * nt;
-        if (k >= total) continue;
-        const double wt = c[u] < dinf() ? exp_noinline(-(c[u] - m0) * inv_lam) : 0.0;
-        const int mm = m[u] < io.M ? m[u] : 0;  // padding slot of the last CTA: weight 0, any valid row
-        mlist[k] = mm;
-        wlist[k] = wt;
-        if (k < kLightMax) {
-          smlist[k] = mm;
-          sc[kFmW + k] = wt;
-        }
-        z += wt;
-        nz += wt != 0.0 ? 1 : 0;
-      }
-    }
   }
+  // (more than kLightMax list entries: the heavy merge below expands them in
+  // parallel over the helper CTAs)
   z = warp_sum_d(z);
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) nz += __shfl_xor_sync(kFull, nz, d);
-  // the record head: written by warp 0 alone for a short list (one barrier),
-  // after a fixed-order sum over the warps otherwise
+  // the record head (warp 0 alone for a short list; after the participants'
+  // partials for the heavy merge)
   auto write_head = [&](double Zs, double NZ) {
     double *dst = io.rank_part;
     dst[0] = m0;
@@ -1316,12 +1341,63 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
     misc[41] = NZ;  // nonzero weights (the only one, if NZ == 1, is the minimum's: sc[kFmBest])
     if (trace_head) trace_head[4] = gtimer();
   };
-  if (total <= 32) {
-    if (tid == 0) write_head(z, (double)nz);
-  } else {
-    if (lane == 0) {  // (misc[16..] and [32..] were last read before the compaction barrier)
-      misc[16 + warp] = z;
-      misc[32 + warp] = (double)nz;
+  if (total <= 32 && tid == 0) write_head(z, (double)nz);
+  __syncthreads();
+  const int ncand = total;  // list length (zero weights included)
+  const bool heavy = ncand > kLightMax;
+  unsigned int *hc = io.counters + (ctas + kGroup - 1) / kGroup + 2;  // merge words (kHc*)
+  const int ph = merge_helpers(io, ctas);
+  if (tid == 0) {  // verdict to the waiting helper CTAs (the lists are published by the barrier + fence)
+    // list length: read by the helpers (heavy) and by vpb_smpc_debug_weights
+    hc[kHcCount] = (unsigned int)ncand;
+    if (heavy) {  // what the participants need to expand their slices of the CTA list
+      const unsigned long long mb = (unsigned long long)__double_as_longlong(m0);
+      hc[kHcM0] = (unsigned int)mb;
+      hc[kHcM0 + 1] = (unsigned int)(mb >> 32);
+      for (int w = 0; w < nw; ++w) hc[kHcWcount + w] = (unsigned int)wcount[w];
+      hc[kHcSpan] = (unsigned int)span;
+      hc[kHcNw] = (unsigned int)nw;
+      hc[kHcList] = (unsigned int)(ncand / NWC);
+      // about nt / 2 candidates per participant: the slice's row loads take a
+      // few round trips while the partials to add stay few
+      const int want = (ncand + nt / 2 - 1) / (nt / 2);
+      hc[kHcParts] = (unsigned int)(want < ph + 1 ? (want > 1 ? want : 1) : ph + 1);
+      fence_acq_rel_gpu();  // helpers read the lists and these words after this release
+    }
+    *reinterpret_cast<volatile unsigned int *>(hc + kHcFlag) = ((ep & 0x3fffffffu) << 2) | (heavy ? 2u : 1u);
+    hc[0] = ep + 1u;  // next launch's epoch (every CTA of this one has read it)
+  }
+  if (heavy) {
+    // this CTA is the last participant; then the partials in participant order
+    __syncthreads();  // (thread 0 published the participants' words above)
+    if (trace_head && tid == 0) trace_head[7] = gtimer();
+    const int P = (int)__ldcg(hc + kHcParts);
+    heavy_part<ET, NWC>(io, S, hc, P - 1, P, hn);
+    __syncthreads();
+    if (trace_head && tid == 0) trace_head[8] = gtimer();
+    if (tid == 0) {
+      SpinGuard g;
+      while (ld_acquire_gpu(hc + kHcDone) != (unsigned int)(P - 1)) g.pause(32);
+      hc[kHcDone] = 0u;
+    }
+    __syncthreads();
+    if (trace_head && tid == 0) trace_head[9] = gtimer();
+    // the partials in participant order: Z and the count by a fixed-shape
+    // block reduction (thread q holds participant q), N element-wise with
+    // the participants' loads in flight together
+    const int Lp = 2 + hn;
+    const double zq = tid < P ? __ldcg(io.hparts + (size_t)tid * Lp) : 0.0;
+    const double nq = tid < P ? __ldcg(io.hparts + (size_t)tid * Lp + 1) : 0.0;
+    const double zw = warp_sum_d(zq), nw_ = warp_sum_d(nq);
+    if (lane == 0) {
+      misc[16 + warp] = zw;
+      misc[32 + warp] = nw_;
+    }
+    for (int e = tid; e < hn; e += nt) {
+      double acc = 0.0;
+#pragma unroll 8
+      for (int q = 0; q < P; ++q) acc += __ldcg(io.hparts + (size_t)q * Lp + 2 + e);
+      io.rank_part[kPartHead + e] = acc;
     }
     __syncthreads();
     if (tid == 0) {
@@ -1331,19 +1407,9 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
         NZ += misc[32 + w];
       }
       write_head(Zs, NZ);
+      if (trace_head) trace_head[10] = gtimer();
     }
-  }
-  __syncthreads();
-  const int ncand = total;  // list length (zero weights included)
-  const bool heavy = ncand > kLightMax;
-  unsigned int *hc = io.counters + (ctas + kGroup - 1) / kGroup + 2;  // merge words (kHc*)
-  const int ph = merge_helpers(io, ctas);
-  if (tid == 0) {  // verdict to the waiting helper CTAs (the lists are published by the barrier + fence)
-    // list length: read by the helpers (heavy) and by vpb_smpc_debug_weights
-    hc[kHcCount] = (unsigned int)ncand;
-    if (heavy) fence_acq_rel_gpu();  // helpers read the lists and the count after this release
-    *reinterpret_cast<volatile unsigned int *>(hc + kHcFlag) = ((ep & 0x3fffffffu) << 2) | (heavy ? 2u : 1u);
-    hc[0] = ep + 1u;  // next launch's epoch (every CTA of this one has read it)
+    __syncthreads();
   }
   if (tid == 32) {
     // record tail: best index and the extension [nonzero count, the single
@@ -1360,20 +1426,11 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   //    (+ U* = nominal + N / Z, clipped command, shifted warm start)
   const ET *eps = reinterpret_cast<const ET *>(io.eps);
   const double Z = sc[kFmRec + 1];
-  if (heavy) {  // this CTA is the last participant; the helpers do the other slices
-    n_slice<ET>(io, S, mlist, wlist, ncand, hn, ph, ph + 1, io.rank_part + kPartHead);
-    if (tid == 0) {
-      SpinGuard g;
-      while (ld_acquire_gpu(hc + kHcDone) != (unsigned int)ph) g.pause(64);
-      hc[kHcDone] = 0u;
-    }
-    __syncthreads();
-  }
 #pragma unroll 1
   for (int e = tid; e < hn; e += nt) {
     double acc = 0.0;
     if (heavy) {
-      acc = __ldcg(io.rank_part + kPartHead + e);
+      acc = io.rank_part[kPartHead + e];  // (this thread's own sum above)
     } else {  // <= kLightMax candidates: smem lists
       const int *ml = smlist;
       const double *wl = sc + kFmW;
@@ -1483,7 +1540,7 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
   if (flag[0] == 0u) return false;
   const unsigned int ep = reinterpret_cast<const unsigned int *>(S.misc + 46)[0];
   if (flag[0] == 3u) {
-    merge_helper<ET>(io, S, ctas, hn, (int)flag[1], ep);
+    merge_helper<ET, NWC>(io, S, ctas, hn, (int)flag[1], ep);
     return false;
   }
   VPB_TRACE(io, 2 * ctas);
@@ -2081,7 +2138,7 @@ static AccLimit acc_of(const vpb_problem *p) {
 }
 
 struct SmpcWs {
-  double *cta_parts, *group_parts, *rank_part, *pro, *cand_costs, *cand_terms;
+  double *cta_parts, *group_parts, *rank_part, *pro, *cand_costs, *cand_terms, *hparts;
   unsigned int *counters;
   size_t bytes;
 };
@@ -2107,6 +2164,8 @@ static SmpcWs smpc_ws(void *base, int64_t M, int64_t H, int64_t n) {
   o += align_up((size_t)NWF * 4 * 8, 256);
   w.counters = reinterpret_cast<unsigned int *>(b + o);
   o += align_up((size_t)(groups + 2 + kHcWords) * 4, 256);  // group counters, ticket, prologue flag, merge words
+  w.hparts = reinterpret_cast<double *>(b + o);  // heavy-merge partials of up to kMergeHelpers + 1 participants
+  o += align_up((size_t)(kMergeHelpers + 1) * (2 + H * n) * 8, 256);
   w.bytes = o;
   return w;
 }
@@ -2202,6 +2261,7 @@ static int smpc_launch(const vpb_problem *prob, const vpb_field *field, const vo
   io.pro = w.pro;
   io.cand_costs = w.cand_costs;
   io.cand_terms = w.cand_terms;
+  io.hparts = w.hparts;
   io.finish = out != nullptr;
   io.out = out;
   io.acc = acc_of(prob);
