@@ -953,7 +953,7 @@ constexpr int kMergeHelpers = 127;
 // merge words after the ticket and the prologue flag: the epoch shares their
 // line (read once per CTA); the polled flag (+ count) and the done counter
 // get lines of their own so the waiting helpers do not contend with them
-constexpr int kHcFlag = 32, kHcCount = 33, kHcDone = 64, kHcStage = 80, kHcWords = 96;
+constexpr int kHcFlag = 32, kHcCount = 33, kHcDone = 64, kHcDone2 = 65, kHcStage = 80, kHcWords = 96;
 // heavy-merge parameters published with the verdict (on the flag's line):
 // the minimum (f64 bits), the per-warp CTA-list lengths, their stride, the
 // merger's warp count, the CTA-list length
@@ -1080,6 +1080,43 @@ __device__ void heavy_part(const SmpcIO &io, const Shared &S, const unsigned int
   }
 }
 
+// Second stage of the heavy merge, by every participant: once all P
+// partials are published (done == P), participant `part` adds, for its slice
+// of the H n elements, the P partials in participant order (thread q holds
+// participant q; fixed-shape block reduction) into N (rank_part), then
+// counts itself in done2.  The merger waits for done2 == P.
+__device__ void heavy_sum_slice(const SmpcIO &io, const Shared &S, unsigned int *hc, int part, int P, int hn) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+  __syncthreads();
+  if (tid == 0) {
+    fence_acq_rel_gpu();  // this participant's partial before its count
+    atomicAdd(hc + kHcDone, 1u);
+    SpinGuard g;
+    while (ld_acquire_gpu(hc + kHcDone) < (unsigned int)P) g.pause(32);
+  }
+  __syncthreads();
+  const int Lp = 2 + hn;
+  const int per = (hn + P - 1) / P;
+  const int e0 = part * per, e1 = min(hn, e0 + per);
+  double *red = reinterpret_cast<double *>(S.centers);  // [nw] (free here)
+  for (int e = e0; e < e1; ++e) {
+    const double v = tid < P ? __ldcg(io.hparts + (size_t)tid * Lp + 2 + e) : 0.0;
+    const double ws = warp_sum_d(v);
+    if (lane == 0) red[warp] = ws;
+    __syncthreads();
+    if (tid == 0) {
+      double acc = 0.0;
+      for (int w = 0; w < nw; ++w) acc += red[w];  // fixed warp order
+      io.rank_part[kPartHead + e] = acc;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    fence_acq_rel_gpu();
+    atomicAdd(hc + kHcDone2, 1u);
+  }
+}
+
 // A helper CTA (one of the last kMergeHelpers finishers): wait for the merge's
 // verdict; on "help", compute slice `part` and report done.
 template <typename ET, int NWC>
@@ -1098,11 +1135,7 @@ __device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn
   const int P = (int)__ldcg(c + kHcParts);  // participants: helpers 0 .. P-2 and the merger
   if (part >= P - 1) return;
   heavy_part<ET, NWC>(io, S, c, part, P, hn);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    fence_acq_rel_gpu();
-    atomicAdd(c + kHcDone, 1u);
-  }
+  heavy_sum_slice(io, S, c, part, P, hn);
 }
 
 // Shared-memory slots of the final merge and the fixed-path tail (S.scratch,
@@ -1373,18 +1406,18 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
     if (trace_head && tid == 0) trace_head[7] = gtimer();
     const int P = (int)__ldcg(hc + kHcParts);
     heavy_part<ET, NWC>(io, S, hc, P - 1, P, hn);
-    __syncthreads();
     if (trace_head && tid == 0) trace_head[8] = gtimer();
+    heavy_sum_slice(io, S, hc, P - 1, P, hn);
     if (tid == 0) {
       SpinGuard g;
-      while (ld_acquire_gpu(hc + kHcDone) != (unsigned int)(P - 1)) g.pause(32);
-      hc[kHcDone] = 0u;
+      while (ld_acquire_gpu(hc + kHcDone2) != (unsigned int)P) g.pause(32);
+      hc[kHcDone] = 0u;  // every participant is past both counters
+      hc[kHcDone2] = 0u;
     }
     __syncthreads();
     if (trace_head && tid == 0) trace_head[9] = gtimer();
-    // the partials in participant order: Z and the count by a fixed-shape
-    // block reduction (thread q holds participant q), N element-wise with
-    // the participants' loads in flight together
+    // Z and the nonzero count: fixed-shape block reduction over the
+    // participants (thread q holds participant q); N is in rank_part
     const int Lp = 2 + hn;
     const double zq = tid < P ? __ldcg(io.hparts + (size_t)tid * Lp) : 0.0;
     const double nq = tid < P ? __ldcg(io.hparts + (size_t)tid * Lp + 1) : 0.0;
@@ -1392,12 +1425,6 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
     if (lane == 0) {
       misc[16 + warp] = zw;
       misc[32 + warp] = nw_;
-    }
-    for (int e = tid; e < hn; e += nt) {
-      double acc = 0.0;
-#pragma unroll 8
-      for (int q = 0; q < P; ++q) acc += __ldcg(io.hparts + (size_t)q * Lp + 2 + e);
-      io.rank_part[kPartHead + e] = acc;
     }
     __syncthreads();
     if (tid == 0) {
@@ -1430,7 +1457,7 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   for (int e = tid; e < hn; e += nt) {
     double acc = 0.0;
     if (heavy) {
-      acc = io.rank_part[kPartHead + e];  // (this thread's own sum above)
+      acc = __ldcg(io.rank_part + kPartHead + e);  // (the participants' sums, acquired above)
     } else {  // <= kLightMax candidates: smem lists
       const int *ml = smlist;
       const double *wl = sc + kFmW;
