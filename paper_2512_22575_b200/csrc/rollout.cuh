@@ -331,7 +331,10 @@ __device__ __forceinline__ bool pose_quad(const Prob<T> &P, const Dyn<T> &D, con
 
 template <typename T>
 __device__ __forceinline__ T bound_violation(T x, T lo, T hi) {
-  return x > hi ? x - hi : (x < lo ? x - lo : T(0));
+  // x - clamp(x, lo, hi): x - hi above, x - lo below, exactly 0 inside (lo <
+  // hi), the same FADD as the reference's branches (vp/batch.py:140-149)
+  if constexpr (sizeof(T) == 4) return x - fminf(fmaxf(x, lo), hi);
+  else return x - fmin(fmax(x, lo), hi);
 }
 
 }  // namespace vpb
