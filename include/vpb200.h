@@ -280,7 +280,10 @@ int vpb_smpc_partial(const vpb_problem *prob, const vpb_field *field,
  *    best_cost, Z, nonfinite_count, best_index, e_pos, e_ori]
  * (e_pos / e_ori: end-effector errors at the start state, vp/planner.py:
  * 620-629; filled by vpb_ee_errors on the host, NaN from the device step)
- * (weighted_cost = +inf when the re-evaluation hits the log singularity). */
+ * (weighted_cost = +inf when the re-evaluation hits the log singularity;
+ * nonfinite_count = samples flagged at the log singularity + 2^32 x samples
+ * with any other non-finite cost: the reference raises DegenerateRotation for
+ * the former, ValueError from soft_weights for the latter). */
 int64_t vpb_smpc_out_len(int64_t H, int64_t n);
 int vpb_smpc_step(const vpb_problem *prob, const vpb_field *field,
                   const void *eps, int dtype, const double *nominal, int64_t M,

@@ -1516,9 +1516,10 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
     const int w = threadIdx.x;
     const int64_t m = cta_m0 + w;
     double c = dinf();
+    bool failed = false;
     if (w < NWC && m < io.M) {
       const double *sm = S.sums + w * 6;
-      const bool failed = S.fail[w] != 0 || S.tfail[w] != 0;
+      failed = S.fail[w] != 0 || S.tfail[w] != 0;
       c = failed ? dinf() : sm[0] + sm[1] + sm[2] + sm[3] + sm[4] + S.cost[w];
       costs[m] = c;
       if (io.flags) io.flags[m] = failed ? 1 : 0;
@@ -1529,7 +1530,11 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
       }
     }
     const bool real = w < NWC && m < io.M;
-    const unsigned nfm = __ballot_sync(kFull, real && !(c < dinf()));
+    // non-finite costs: the reference's flagged samples (DegenerateRotation,
+    // vp/planner.py:540-546) counted apart from any other non-finite cost
+    // (ValueError in soft_weights): count = flagged + 2^32 other
+    const unsigned fmk = __ballot_sync(kFull, real && failed);
+    const unsigned omk = __ballot_sync(kFull, real && !failed && !(c < dinf()));
     double mn = c;
     int bi = real ? w : 0x7fffffff;
 #pragma unroll
@@ -1547,7 +1552,7 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
     __syncwarp();
     if (w == 0) {
       heads[cta] = mn;
-      heads[ctas + cta] = (double)__popc(nfm);
+      heads[ctas + cta] = (double)__popc(fmk) + 4294967296.0 * (double)__popc(omk);
       heads[2 * (size_t)ctas + cta] = mn < dinf() ? (double)(io.m_offset + cta_m0 + bi) : -1.0;
       // publication: one gpu-scope release fence + the counter atomic; the
       // CTA taking the last ticket acquires before reading the others' heads

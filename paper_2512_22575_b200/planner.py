@@ -439,8 +439,12 @@ class Planner:
         # [cost(U*), 5 sums, terminal, best, Z, non-finite, best index, e_pos, e_ori] as Python floats
         v = out_host[base:base + 13].tolist()
         wcost = v[0]
-        if v[9] > 0 or not math.isfinite(wcost):
+        # non-finite count = flagged samples + 2^32 x other non-finite costs (rollout.cu)
+        flagged = math.fmod(v[9], 4294967296.0)
+        if flagged > 0 or not math.isfinite(wcost):
             raise DegenerateRotation("a sample reached a pose error with rotation angle at pi")
+        if v[9] > 0:
+            raise ValueError("costs must be finite")  # vp/planner.py:377-378 (soft_weights)
         if not math.isfinite(v[11]):  # device-step output: diagnostics on the host
             q0 = np.ascontiguousarray(state.q, dtype=np.float64)
             gr = np.ascontiguousarray(goal.rotation.matrix, dtype=np.float64)
