@@ -41,6 +41,7 @@ namespace vpb {
 constexpr int NW = 8;                    // candidate warps per CTA (generic path, rollout kernel)
 constexpr int NWF = 4;                   // candidate warps per CTA of the fixed-topology SMPC kernel
 constexpr int kThreads = (NW + 1) * 32;  // + terminal warp
+#define VPB_NOM_INLINE 512  // H n of the parameter-carried nominal (session path)
 constexpr int kPartHead = 4;             // [m, Z, nonfinite, best_index]
 constexpr int kPartExt = 7;              // after N: [nonzero-weight count, the single candidate's 6 sums]
 constexpr int kGroup = 32;               // CTAs merged by a group's last CTA
@@ -839,6 +840,15 @@ struct SmpcIO {
   int stage_len;
 };
 
+// Session (fused fixed path, smpc_kernel<..., INL = true>): the nominal
+// inline in the launch parameters, copied into shared memory by every CTA.
+// The other instantiations carry a one-element stub.
+template <bool INL>
+struct NomInline {
+  double v[INL ? VPB_NOM_INLINE : 1];
+  int n;
+};
+
 // U* = nominal + N / Z, the clipped command and the shifted warm start
 // (vp/planner.py:614-619), written to `out` by all threads of the CTA.
 __device__ __forceinline__ void tail_controls(const double *part, const double *nominal, const AccLimit &acc, int H,
@@ -1166,7 +1176,8 @@ constexpr int kFmCap = 16;
 // warm start are produced in the N pass itself (to out and out_host).
 template <typename ET, int NWC, bool FIXED>
 __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *heads, const double *costs, int ctas,
-                            int hn, int nj, bool fused_u, unsigned int ep, unsigned long long *trace_head) {
+                            int hn, int nj, bool fused_u, unsigned int ep, unsigned long long *trace_head,
+                            const double *nominal) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   double *misc = S.misc;
   double *sc = S.scratch;
@@ -1177,7 +1188,7 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   int *smlist = reinterpret_cast<int *>(sc + kFmML);
   const double inv_lam = 1.0 / io.lam;
   if (fused_u) {  // the nominal is read by the U* pass at the end: start it towards L2 now
-    for (int e = tid * 16; e < hn; e += nt * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(io.nominal + e));
+    for (int e = tid * 16; e < hn; e += nt * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(nominal + e));
   }
   // 1. global minimum over the CTA heads (first CTA attaining it)
   constexpr int kHR = 8;  // heads kept in registers per lane (ctas <= nw * 32 * kHR)
@@ -1475,7 +1486,7 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
       io.rank_part[kPartHead + e] = acc;
     }
     if (fused_u) {  // tail_controls, element e
-      const double u = io.nominal[e] + acc / Z;
+      const double u = nominal[e] + acc / Z;
       const int64_t o2 = (int64_t)hn + e;  // clipped command (e < nj) / shifted warm start
       double v2 = u;
       if (e < nj) {
@@ -1504,7 +1515,7 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
 // final merge.  Returns true on the CTA that merged.
 template <typename ET, int NWC, bool FIXED>
 __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t cta_m0, int hn, int nj, int cta,
-                                     int ctas) {
+                                     int ctas, const double *nominal) {
   const int groups = (ctas + kGroup - 1) / kGroup;
   double *heads = io.cta_parts;  // [3][ctas]
   double *costs = io.costs ? io.costs : io.cand_costs;
@@ -1577,7 +1588,7 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
   }
   VPB_TRACE(io, 2 * ctas);
   final_merge<ET, NWC, FIXED>(io, S, heads, costs, ctas, hn, nj, FIXED && io.finish, ep,
-                              io.trace ? io.trace + 2 * ctas + 13 : nullptr);
+                              io.trace ? io.trace + 2 * ctas + 13 : nullptr, nominal);
   if (threadIdx.x == 0) io.counters[groups] = 0u;
   VPB_TRACE(io, 2 * ctas + 1);
   return true;
@@ -1611,9 +1622,10 @@ __device__ __forceinline__ void stage_inputs(const SmpcIO &io, int ctas) {
 
 // Fused SMPC step: rollout -> CTA partial -> group merge -> global merge
 // [-> U*, clip, shift, re-evaluation].
-template <typename T, typename ET, int MAXJ, typename Topo>
+template <typename T, typename ET, int MAXJ, typename Topo, bool INL = false>
 __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>())
-    smpc_kernel(const __grid_constant__ Prob<T> P, const __grid_constant__ SmpcIO io) {
+    smpc_kernel(const __grid_constant__ Prob<T> P, const __grid_constant__ SmpcIO io,
+                const __grid_constant__ NomInline<INL> nin) {
 #ifdef VPB_SMEM_SPILL
   // the fixed path's layout is a compile-time constant: static shared memory,
   // and the register spills of the 72-register budget go to shared memory
@@ -1633,8 +1645,16 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
   const SmemLayout L = smem_layout(is_dyn_v<Topo> ? P.ns : 0, sizeof(T), kMergeScratch);
   const Shared S = carve(smem_raw, L);
   Dyn<T> &D = *reinterpret_cast<Dyn<T> *>(S.dyn);
+  const double *nominal = io.nominal;
   if constexpr (!is_dyn_v<Topo>) {
     if (io.stage_src) stage_inputs(io, (int)gridDim.x - 1);
+    if constexpr (INL) {
+      // session: the nominal rides in the launch parameters; each CTA copies
+      // it to shared memory (ordered by the barrier below) and reads it there
+      __shared__ double nom_s[VPB_NOM_INLINE];
+      for (int i = threadIdx.x; i < nin.n; i += blockDim.x) nom_s[i] = nin.v[i];
+      nominal = nom_s;
+    }
   }
   if (threadIdx.x < 32) load_dyn<T>(P, io.dyn, D);
   __syncthreads();
@@ -1645,7 +1665,9 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
     VPB_TRACE(io, 2 * blockIdx.x);
     CandOut co{nullptr, nullptr, nullptr};
     evaluate_cta<T, ET, MAXJ>(P, D, eps, io.nominal, io.M, cta_m0, S, co);
-    if (!cta_reduce_and_merge<ET, smpc_nw<Topo>(), false>(io, S, cta_m0, hn, P.nj, blockIdx.x, gridDim.x)) return;
+    if (!cta_reduce_and_merge<ET, smpc_nw<Topo>(), false>(io, S, cta_m0, hn, P.nj, blockIdx.x, gridDim.x,
+                                                         io.nominal))
+      return;
     if (io.finish) {
       smpc_tail_dyn<T, MAXJ>(P, D, io.rank_part, io.nominal, io.acc, io.out, S);
       if (io.out_host) {
@@ -1672,7 +1694,7 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
       const int64_t m = cm0 + warp;
       const bool cand = state == 1;
       const ET *ctrl = (cand && m < io.M) ? eps + (size_t)m * hn : nullptr;
-      const double *nom = state == 1 ? io.nominal : (state == 2 ? io.out : nullptr);
+      const double *nom = state == 1 ? nominal : (state == 2 ? io.out : nullptr);
       fixed_candidate<T, ET, Topo>(P, D, io.gen_on ? nullptr : ctrl, nom, cand ? m < io.M : true,
                                    state == 0 ? 1 : P.H, state == 0 ? 0 : 1, cand ? 0 : warp, cand ? 1 : NWF,
                                    S.sums + warp * 6, S.cost + warp, S.fail + warp,
@@ -1698,7 +1720,7 @@ __global__ void __launch_bounds__(smpc_threads<Topo>(), smpc_min_blocks<T, Topo>
       VPB_TRACE(io, 2 * cta + 1);
       // (the final merge also fetched the q_0 terms into S.pro and, when
       // finishing, wrote U*, the command and the warm start)
-      if (!cta_reduce_and_merge<ET, smpc_nw<Topo>(), true>(io, S, cm0, hn, P.nj, cta, ncta)) return;
+      if (!cta_reduce_and_merge<ET, smpc_nw<Topo>(), true>(io, S, cm0, hn, P.nj, cta, ncta, nominal)) return;
       if (!io.finish) {
         fixed_shard_fixup(S, io.M, io.costs, io.flags, io.rank_part);
         return;
@@ -2111,7 +2133,7 @@ static int launch_smpc_t(const Prob<T> &P, const SmpcIO &io, int topo, cudaStrea
 #else
     const size_t dsm = smem;
 #endif
-    k<<<(unsigned)ctas, threads, dsm, s>>>(P, io2);
+    k<<<(unsigned)ctas, threads, dsm, s>>>(P, io2, NomInline<false>{});
   };
 #ifdef VPB_QUICK
   if constexpr (!std::is_same_v<T, float> || !std::is_same_v<ET, float>) return VPB_ERR_ARG;
@@ -2432,6 +2454,113 @@ int smpc_generate_session(const vpb_problem *prob, const vpb_field *field, const
   return smpc_launch(prob, field, eps_out, dtype, nominal, M, 0, precision, nullptr, nullptr, nullptr, out, workspace,
                      workspace_bytes, s, nullptr, true, out_host);
 }
+
+// Session launch of the fused fp32 fixed-topology step with the per-call
+// state in the launch parameters: q0, qd0, goal in Prob, the seed in the
+// noise generator, the field pointer in Prob, the nominal inline in SmpcIO.
+// Built once per session, patched every step (smpc_session_node_patch).
+struct SmpcNode {
+  Prob<float> P;
+  SmpcIO io;
+  NomInline<true> nin;
+  void *args[3];
+  cudaKernelNodeParams np;
+  int nj, hn;
+};
+
+int smpc_session_node(const vpb_problem *prob, const vpb_field *field, int64_t window, const double *sigma,
+                      int64_t M, int precision, void *eps_out, double *out, double *out_host, void *workspace,
+                      size_t workspace_bytes, SmpcNode **res) {
+  *res = nullptr;
+  const bool fused = precision == VPB_PREC_F32 && window <= 5 && !fixed_topology_disabled() && topo_id(prob) == 1 &&
+                     (int64_t)prob->horizon * prob->n_joints <= VPB_NOM_INLINE;
+  if (!fused || getenv("VPB_SESSION_STAGE")) return VPB_OK;  // the caller stages the per-call block instead
+  int rc = prob_checks(prob, precision, VPB_DTYPE_F32);
+  if (rc) return rc;
+  VPB_REQUIRE(prob->lam > 0.0, "temperature must be positive");
+  const int64_t H = prob->horizon, n = prob->n_joints;
+  VPB_REQUIRE(M >= 1 && M <= ((int64_t)1 << 31) * NWF, "bad sample count");
+  const SmpcWs w = smpc_ws(workspace, M, H, n);
+  VPB_REQUIRE(workspace && workspace_bytes >= w.bytes, "workspace too small");
+  vpb_problem pb = *prob;
+  pb.dyn_state = nullptr;  // the per-call state travels in the launch parameters
+  pb.field_sq_dev = nullptr;
+  auto *nd = new SmpcNode();
+  memset(nd, 0, sizeof(*nd));
+  if ((rc = build_prob<float>(&pb, field, nd->P))) {
+    delete nd;
+    return rc;
+  }
+  SmpcIO &io = nd->io;
+  io.eps = eps_out;
+  io.nominal = nullptr;  // (the INL kernel reads nin instead)
+  io.M = M;
+  io.lam = prob->lam;
+  io.cta_parts = w.cta_parts;
+  io.group_parts = w.group_parts;
+  io.counters = w.counters;
+  io.rank_part = w.rank_part;
+  io.pro = w.pro;
+  io.cand_costs = w.cand_costs;
+  io.cand_terms = w.cand_terms;
+  io.hparts = w.hparts;
+  io.finish = 1;
+  io.out = out;
+  io.acc = acc_of(prob);
+  io.trace = g_smpc_trace;
+  io.out_host = out_host;
+  nd->nin.n = (int)(H * n);
+  io.gen.window = (int)window;
+  for (int64_t j = 0; j < n; ++j) io.gen.sigma[j] = (float)sigma[j];
+  io.gen_on = 1;
+  io.eps_out = reinterpret_cast<float *>(eps_out);
+  auto k = smpc_kernel<float, float, 8, TopoRobot7, true>;
+  const size_t smem = smem_bytes(nd->P, kMergeScratch, 1);
+  if ((rc = set_smem(k, smem))) {
+    delete nd;
+    return rc;
+  }
+  const int threads = smpc_threads<TopoRobot7>();
+  const int slots = resident_slots(k, threads, smem);
+  io.max_helpers = slots - 2 < kMergeHelpers ? (slots - 2 > 0 ? slots - 2 : 0) : kMergeHelpers;
+#ifdef VPB_SMEM_SPILL
+  const size_t dsm = 0;
+#else
+  const size_t dsm = smem;
+#endif
+  nd->args[0] = &nd->P;
+  nd->args[1] = &nd->io;
+  nd->args[2] = &nd->nin;
+  nd->np.func = reinterpret_cast<void *>(k);
+  nd->np.gridDim = dim3((unsigned)(ceil_div(M, NWF) + 1));
+  nd->np.blockDim = dim3((unsigned)threads);
+  nd->np.sharedMemBytes = (unsigned)dsm;
+  nd->np.kernelParams = nd->args;
+  nd->np.extra = nullptr;
+  nd->nj = (int)n;
+  nd->hn = (int)(H * n);
+  *res = nd;
+  return VPB_OK;
+}
+
+void smpc_session_node_patch(SmpcNode *nd, const double *q0, const double *qd0, const double *goal_r,
+                             const double *goal_t, const double *nominal, uint64_t seed, const float *sq) {
+  for (int j = 0; j < nd->nj; ++j) {
+    nd->P.q0[j] = (float)q0[j];
+    nd->P.qd0[j] = (float)qd0[j];
+  }
+  for (int a = 0; a < 9; ++a) nd->P.goal_r[a] = (float)goal_r[a];
+  for (int a = 0; a < 3; ++a) nd->P.goal_t[a] = (float)goal_t[a];
+  if (nd->P.has_field && sq) nd->P.sq = sq;
+  if (nominal) memcpy(nd->nin.v, nominal, (size_t)nd->hn * 8);
+  else memset(nd->nin.v, 0, (size_t)nd->hn * 8);
+  nd->io.gen.seed = seed;
+}
+
+const cudaKernelNodeParams *smpc_session_node_params(const SmpcNode *nd) { return &nd->np; }
+
+void smpc_session_node_free(SmpcNode *nd) { delete nd; }
+
 }  // namespace vpb
 
 extern "C" {

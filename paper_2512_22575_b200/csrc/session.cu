@@ -26,6 +26,9 @@ struct vpb_smpc_session {
   double sigma[VPB_MAX_JOINTS];
   cudaStream_t stream;
   cudaGraphExec_t exec;
+  vpb::SmpcNode *node;     // fused fp32 path: the step kernel's parameters (per-call state patched in)
+  cudaGraphNode_t gnode;   // its kernel node in `exec`
+  bool direct;             // re-parameterising the node failed: launch the kernel directly
   cudaEvent_t launched;  // recorded after an asynchronous vpb_smpc_session_launch
   bool inflight;         // a launch() replay may still read h_in / write h_out
   double *h_in, *d_in;  // [dyn (2n + 12) | seed bits | field pointer bits | nominal (H n)]
@@ -42,6 +45,7 @@ void release(vpb_smpc_session *s) {
   if (s->inflight) cudaEventSynchronize(s->launched);
   if (s->launched) cudaEventDestroy(s->launched);
   if (s->exec) cudaGraphExecDestroy(s->exec);
+  if (s->node) vpb::smpc_session_node_free(s->node);
   if (s->stream) cudaStreamDestroy(s->stream);
   cudaFreeHost(s->h_in);
   cudaFreeHost(s->h_out);
@@ -61,6 +65,18 @@ int enqueue(vpb_smpc_session *s, bool copies) {
                                     s->window, s->sigma, s->d_in + nom, s->M, s->precision, s->eps, s->d_out,
                                     s->h_out, s->ws, s->ws_bytes, s->stream, copies ? s->h_in : nullptr, s->d_in,
                                     s->in_len);
+}
+
+// Fused fp32 path: replay the one-node graph with this step's parameters
+// (or, if the node cannot be re-parameterised, launch the kernel directly).
+cudaError_t launch_node(vpb_smpc_session *s, cudaStream_t st, bool reparam) {
+  const cudaKernelNodeParams *np = vpb::smpc_session_node_params(s->node);
+  if (!s->direct && reparam && cudaGraphExecKernelNodeSetParams(s->exec, s->gnode, np) != cudaSuccess) {
+    cudaGetLastError();
+    s->direct = true;
+  }
+  if (s->direct) return cudaLaunchKernel(np->func, np->gridDim, np->blockDim, np->kernelParams, np->sharedMemBytes, st);
+  return cudaGraphLaunch(s->exec, st);
 }
 
 // 3x3 row-major helpers (host, double)
@@ -197,6 +213,32 @@ int vpb_smpc_session_create(const vpb_problem *prob, const vpb_field *field, int
   memcpy(s->h_in + s->dyn_len + 1, &sq0, sizeof(sq0));
   s->prob.dyn_state = s->d_in;
   s->prob.field_sq_dev = reinterpret_cast<const float *const *>(s->d_in + s->dyn_len + 1);
+  // fused fp32 path: no per-call copy at all -- state, goal, seed, field
+  // pointer and nominal ride in the step kernel's launch parameters
+  rc = vpb::smpc_session_node(prob, field ? &s->field : nullptr, window, sigma, M, precision, s->eps, s->d_out,
+                              s->h_out, s->ws, s->ws_bytes, &s->node);
+  if (rc) {
+    release(s);
+    return rc;
+  }
+  if (s->node) {
+    const double *h = s->h_in;
+    vpb::smpc_session_node_patch(s->node, h, h + s->n, h + 2 * s->n, h + 2 * s->n + 9, nullptr, 0, s->field.sq);
+    cudaGraph_t g = nullptr;
+    SESSION_CUDA(cudaGraphCreate(&g, 0));
+    const cudaError_t ae = cudaGraphAddKernelNode(&s->gnode, g, nullptr, 0, vpb::smpc_session_node_params(s->node));
+    const cudaError_t ie = ae == cudaSuccess ? cudaGraphInstantiate(&s->exec, g, 0) : ae;
+    cudaGraphDestroy(g);
+    if (getenv("VPB_SESSION_DIRECT")) s->direct = true;
+    if (ie != cudaSuccess) {
+      cudaGetLastError();
+      s->direct = true;
+    }
+    SESSION_CUDA(launch_node(s, s->stream, false));  // warm-up
+    SESSION_CUDA(cudaStreamSynchronize(s->stream));
+    *out = s;
+    return VPB_OK;
+  }
   // warm-up outside capture (kernel attributes), then capture the step
   SESSION_CUDA(cudaMemcpyAsync(s->d_in, s->h_in, (size_t)s->in_len * 8, cudaMemcpyHostToDevice, s->stream));
   if ((rc = enqueue(s, false))) {
@@ -252,7 +294,12 @@ int vpb_smpc_session_step(vpb_smpc_session *s, const double *q0, const double *q
   cudaStream_t st = vpb::as_stream(stream);
   volatile uint64_t *done = reinterpret_cast<volatile uint64_t *>(s->h_out + s->out_len);
   *done = 0;  // the previous launch set it as its last action
-  VPB_CUDA(cudaGraphLaunch(s->exec, st));
+  if (s->node) {
+    vpb::smpc_session_node_patch(s->node, q0, qd0, goal_r, goal_t, nominal, seed, sq);
+    VPB_CUDA(launch_node(s, st, true));
+  } else {
+    VPB_CUDA(cudaGraphLaunch(s->exec, st));
+  }
   double e_pos = 0.0, e_ori = 0.0;  // host diagnostics while the step runs
   vpb_ee_errors(&s->prob, q0, goal_r, goal_t, &e_pos, &e_ori);
   // The kernel's last CTA writes the result into pinned memory and then the
@@ -285,7 +332,8 @@ int vpb_smpc_session_launch(vpb_smpc_session *s, void *stream) {
   // (replays of this graph are ordered on the stream and none rewrites h_in,
   // so back-to-back launches need no wait; step() waits for the last one)
   cudaStream_t st = vpb::as_stream(stream);
-  VPB_CUDA(cudaGraphLaunch(s->exec, st));
+  if (s->node) VPB_CUDA(launch_node(s, st, false));
+  else VPB_CUDA(cudaGraphLaunch(s->exec, st));
   VPB_CUDA(cudaEventRecord(s->launched, st));
   s->inflight = true;
   vpb::note_launch(1);

@@ -52,6 +52,18 @@ int smpc_generate_session(const vpb_problem *prob, const vpb_field *field, const
                           double *out, double *out_host, void *workspace, size_t workspace_bytes,
                           cudaStream_t s, const double *stage_src, double *stage_dst, int64_t stage_len);
 
+// Fused fp32 fixed-topology session step with the per-call state in the
+// launch parameters (rollout.cu): built once, patched every step, launched as
+// a graph kernel node.  *node stays null when the path does not apply.
+struct SmpcNode;
+int smpc_session_node(const vpb_problem *prob, const vpb_field *field, int64_t window, const double *sigma,
+                      int64_t M, int precision, void *eps_out, double *out, double *out_host, void *workspace,
+                      size_t workspace_bytes, SmpcNode **node);
+void smpc_session_node_patch(SmpcNode *node, const double *q0, const double *qd0, const double *goal_r,
+                             const double *goal_t, const double *nominal, uint64_t seed, const float *sq);
+const cudaKernelNodeParams *smpc_session_node_params(const SmpcNode *node);
+void smpc_session_node_free(SmpcNode *node);
+
 }  // namespace vpb
 
 #define VPB_REQUIRE(cond, ...)      \
