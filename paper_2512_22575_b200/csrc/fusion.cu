@@ -310,11 +310,40 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   int4 *q = queue[threadIdx.x >> 5];
   int qn = 0;  // warp-uniform queue length
-  for (int64_t li = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); li < lines; li += warps) {
+  // Rounds of blockDim lines per CTA, interleaved over the CTAs (line
+  // r0 + blockIdx + t * gridDim for thread t): every thread solves one line's
+  // z-intervals (the analytic frustum clip, SIMT-parallel instead of 32 lanes
+  // repeating it), the non-empty lines are compacted in thread order, then
+  // the warps take them round robin.
+  __shared__ int s_line[256];
+  __shared__ int4 s_iv[256];
+  __shared__ int s_wcnt[8];
+  const int warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  (void)warps;
+  for (int64_t r0 = 0; r0 < lines; r0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t myli = r0 + blockIdx.x + (int64_t)threadIdx.x * gridDim.x;
+    Interval mia{1, 0}, mim{1, 0};
+    if (myli < lines) line_intervals(A, F, F.xlo + myli / ny, F.ylo + myli % ny, mia, mim);
+    const bool nonempty = mia.lo <= mia.hi || mim.lo <= mim.hi;
+    const unsigned bal = __ballot_sync(kFull, nonempty);
+    if (lane == 0) s_wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int base = 0, total = 0;
+    for (int w = 0; w < nwarp; ++w) {
+      base += w < warp ? s_wcnt[w] : 0;
+      total += s_wcnt[w];
+    }
+    if (nonempty) {
+      const int pos = base + __popc(bal & ((1u << lane) - 1u));
+      s_line[pos] = (int)myli;
+      s_iv[pos] = make_int4(mia.lo, mia.hi, mim.lo, mim.hi);
+    }
+    __syncthreads();
+  for (int le = warp; le < total; le += nwarp) {
+    const int64_t li = s_line[le];
+    const int4 iv = s_iv[le];
     const int64_t x = F.xlo + li / ny, y = F.ylo + li % ny;
-    Interval ia, im;
-    line_intervals(A, F, x, y, ia, im);
-    if (ia.lo > ia.hi && im.lo > im.hi) continue;
+    Interval ia{iv.x, iv.y}, im{iv.z, iv.w};
     // ---- line constants of the conservative fp32 prefilter ----
     // Decides, with explicit error bounds, the voxels whose reference result
     // is certainly "skip" (behind the camera, outside the image, or landing
@@ -468,6 +497,8 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
         flush_exact(A, q, qn, lane, false);
       }
     }
+  }
+    __syncthreads();  // the round's line list is reused by the next round
   }
   __syncwarp();
   flush_exact(A, q, qn, lane, true);
