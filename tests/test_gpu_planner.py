@@ -229,8 +229,8 @@ def test_smpc_step_vs_golden(pk, precision):
         np.testing.assert_allclose(res.diagnostics.e_ori, diag[3], rtol=1e-9, atol=1e-12)
 
 
-@pytest.mark.parametrize("samples", [4096, 16384])
-def test_all_nonzero_weights_step_equals_explicit_update(pk, samples):
+@pytest.mark.parametrize("samples,generic", [(4096, "0"), (16384, "0"), (3000, "1")])
+def test_all_nonzero_weights_step_equals_explicit_update(pk, samples, generic, monkeypatch):
     """Every weight nonzero (lam = 1e4): the fused step's U* (helper-CTA N
     reduction) equals soft_weights + update_controls on the same costs, for
     the one-launch step and for repeated native-session steps (per-launch
@@ -238,6 +238,8 @@ def test_all_nonzero_weights_step_equals_explicit_update(pk, samples):
     pkg, config, mapping, planner, robot = pk
     from paper_2512_22575_b200.geometry import RigidTransform
 
+    # generic = "1": the runtime-topology kernel (8 candidates per CTA) takes the heavy merge too
+    monkeypatch.setenv("VPB_GENERIC_ROLLOUT", generic)
     chain, model = config.robot_7dof()
     params = config.planner_params(7, {"samples": samples, "horizon": 32, "lam": 1e4})
     pl = planner.Planner(chain, model, params, "fp32")
