@@ -1188,7 +1188,8 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
   int *smlist = reinterpret_cast<int *>(sc + kFmML);
   const double inv_lam = 1.0 / io.lam;
   if (fused_u) {  // the nominal is read by the U* pass at the end: start it towards L2 now
-    for (int e = tid * 16; e < hn; e += nt * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(nominal + e));
+    if (__isGlobal(nominal))  // (the session's nominal lives in shared memory)
+      for (int e = tid * 16; e < hn; e += nt * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(nominal + e));
   }
   // 1. global minimum over the CTA heads (first CTA attaining it)
   constexpr int kHR = 8;  // heads kept in registers per lane (ctas <= nw * 32 * kHR)
