@@ -1566,12 +1566,20 @@ __device__ bool cta_reduce_and_merge(const SmpcIO &io, const Shared &S, int64_t 
       heads[cta] = mn;
       heads[ctas + cta] = (double)__popc(fmk) + 4294967296.0 * (double)__popc(omk);
       heads[2 * (size_t)ctas + cta] = mn < dinf() ? (double)(io.m_offset + cta_m0 + bi) : -1.0;
-      // publication: one gpu-scope release fence + the counter atomic; the
-      // CTA taking the last ticket acquires before reading the others' heads
+      // publication: the ticket is an acquire-release atomic at gpu scope --
+      // it releases this CTA's head (and, cumulatively, the lanes' writes
+      // ordered by the __syncwarp above) and, for the CTA taking the last
+      // ticket, acquires every other CTA's
+#ifdef VPB_FENCED_TICKET
       fence_acq_rel_gpu();
       const unsigned int prev = atomicAdd(&io.counters[groups], 1u);
       const bool last = prev == (unsigned int)(ctas - 1);
       if (last) fence_acq_rel_gpu();
+#else
+      unsigned int prev;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&io.counters[groups]) : "memory");
+      const bool last = prev == (unsigned int)(ctas - 1);
+#endif
       const int ph = merge_helpers(io, ctas);
       const bool helper = !last && (int)prev >= ctas - 1 - ph;
       flag[0] = last ? 1u : (helper ? 3u : 0u);
