@@ -28,6 +28,14 @@ int sm_count() {
   return cached;
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("VPB_NO_PDL");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 }  // namespace vpb
 
 extern "C" {

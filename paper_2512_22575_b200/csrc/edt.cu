@@ -736,6 +736,8 @@ __global__ void __launch_bounds__(32 * KSEG) edt_zy_kernel(const uint32_t *__res
   const bool aligned = (lo2 & 31) == 0;
   const int y0 = warp * B, y1 = min(n1, y0 + B);
   const uint32_t stk = tile_s + 4u * (uint32_t)lane + 128u * (uint32_t)y0;
+  pdl_release();
+  pdl_wait();  // the occupancy bits come from the fusion; the g tile buffer may still be read by the last X pass
   const int items = gz * n0;
   for (int item = blockIdx.x; item < items; item += gridDim.x) {
     const int zc = zc_base + item % gz;
@@ -851,6 +853,8 @@ __global__ void __launch_bounds__(32 * KSEG) edt_x_kernel(const __grid_constant_
   const uint32_t col = tile_s + 4u * (uint32_t)lane;
   const uint32_t stk = col + 128u * (uint32_t)q0;
   const int box = ncopies == 1 ? n0 : kTmaRows;
+  pdl_release();
+  pdl_wait();  // g comes from edt_zy_kernel
   if (tid == 0) mbar_init(bar, 1);
   __syncthreads();
   const int items = gz * n1;
@@ -980,16 +984,21 @@ static int edt_tiled(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
   const int occ_zy = cache.occ_zy, occ_x = cache.occ_x;
   const int64_t slots_zy = (int64_t)sm_count() * (occ_zy > 0 ? occ_zy : 1);
   const int64_t slots_x = (int64_t)sm_count() * (occ_x > 0 ? occ_x : 1);
+  // VPB_EDT_PDL: 0 none (default), 1 the Z+Y pass launched under the fusion's tail, 2 also X under
+  // Z+Y.  Measured on the replan: 1 costs 1-2 us and 2 costs 11 us (the early-resident waiting CTAs
+  // slow the running grid more than the hidden launch saves); the fusion pair gains 2 us.
+  static const int pdl_mode = getenv("VPB_EDT_PDL") ? atoi(getenv("VPB_EDT_PDL")) : 0;
+  const bool pdl_zy = pdl_enabled() && pdl_mode >= 1, pdl_x = pdl_enabled() && pdl_mode >= 2;
   for (int z0 = 0; z0 < zch; z0 += group) {
     const int gz = z0 + group <= zch ? group : zch - z0;
     const int64_t it_zy = (int64_t)gz * n[0], it_x = (int64_t)gz * n[1];
-    kzy<<<(unsigned)(it_zy < slots_zy ? it_zy : slots_zy), 32 * KS, smem_zy, s>>>(
-        grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], (int)lo[2], (int)n[0], (int)n[1],
-        (int)n[2], z0, gz, g2);
+    VPB_CUDA(launch_ex(pdl_zy, kzy, dim3((unsigned)(it_zy < slots_zy ? it_zy : slots_zy)), dim3(32 * KS), smem_zy, s,
+                        grid->occ_bits, grid->dims[1], ceil_div(grid->dims[2], 32), lo[0], lo[1], (int)lo[2],
+                        (int)n[0], (int)n[1], (int)n[2], z0, gz, g2));
     rc = check_launch("edt_zy_kernel");
     if (rc) return rc;
-    kx<<<(unsigned)(it_x < slots_x ? it_x : slots_x), 32 * KS, smem_x, s>>>(gmap, (int)n[0], (int)n[1], (int)n[2], z0,
-                                                                             gz, out_sq);
+    VPB_CUDA(launch_ex(pdl_x, kx, dim3((unsigned)(it_x < slots_x ? it_x : slots_x)), dim3(32 * KS), smem_x, s, gmap,
+                        (int)n[0], (int)n[1], (int)n[2], z0, gz, out_sq));
     rc = check_launch("edt_x_kernel");
     if (rc) return rc;
   }

@@ -33,6 +33,7 @@ struct FusionArgs {
   int64_t width, height;
   const double *depth;
   const uint8_t *pixel_masked;
+  const float *pixf;  // optional (vpb_update_occupancy): usable return depth in fp32, NaN if not usable
   double tau, l_hit, l_miss, l_min, l_max, l_thr;
   int n_mask;
   double aabb_lo[3], aabb_hi[3];
@@ -297,9 +298,16 @@ __device__ __forceinline__ void flush_exact(const FusionArgs &A, int4 *q, int &q
 
 // Persistent: each warp takes (x, y) lines of the footprint; per line the
 // 32-voxel words overlapping its intervals run the per-voxel prefilter.
-__global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ FusionArgs A) {
+#ifdef VPB_FUSE_MINB
+#define VPB_FUSE_BOUNDS __launch_bounds__(256, VPB_FUSE_MINB)
+#else
+#define VPB_FUSE_BOUNDS __launch_bounds__(256)
+#endif
+__global__ void VPB_FUSE_BOUNDS fuse_kernel(const __grid_constant__ FusionArgs A) {
   __shared__ Frustum Fs;
   __shared__ int4 queue[8][kFuseQueue];
+  pdl_release();
+  pdl_wait();  // the pixel codes and the usable rectangle come from masked_pixels_kernel
   if (threadIdx.x == 0) frustum_setup(A, Fs);
   __syncthreads();
   const Frustum F = Fs;
@@ -374,6 +382,11 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
       }
       const int64_t z = wz * 32 + lane;
       const bool in_box = (z >= A.lo2) && (z < A.lo2 + A.n2);
+      const int64_t g = gline + z;
+      // the old log-odds, loaded before the classification needs it (one
+      // coalesced 256 B read per word, overlapping the pixel load instead of
+      // following it)
+      const double old = in_box ? A.log_odds[g] : 0.0;
       bool exact = false;
       int fast = 0;  // 1 = certain hit, 2 = certain miss (fp32 classification)
       if (in_box) {
@@ -420,16 +433,21 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
               } else {
                 const int pix = (int)fv * (int)A.width + (int)fu;
                 bool usable;
-                if (A.usable) {
+                float mf;
+                if (A.pixf) {  // one 4-byte load: usable <=> not NaN
+                  mf = __ldg(A.pixf + pix);
+                  usable = mf == mf;
+                } else if (A.usable) {
                   usable = __ldg(A.pixel_masked + pix) == 2;
+                  mf = usable ? (float)__ldg(A.depth + pix) : 0.0f;
                 } else {
                   const double m = __ldg(A.depth + pix);
                   usable = (__ldg(A.pixel_masked + pix) & 1) == 0 && m >= A.d_min && m <= A.d_max;
+                  mf = (float)m;
                 }
                 if (usable) {
                   // classification |qz - D| <= tau (hit) / qz < D - tau (miss) /
                   // occluded, decided in fp32 when clear of both boundaries
-                  const float mf = (float)__ldg(A.depth + pix);
                   const float dd = qzf - mf;
                   const float e = dq + 2e-7f * (fabsf(mf) + A.tauf) + 1e-6f;
                   if (fabsf(dd) <= A.tauf - e) fast = 1;
@@ -445,14 +463,12 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
       }
       bool touched = false;
       double newval = 0.0;
-      const int64_t g = gline + z;
       if (fast == 3) {
-        const double old = A.log_odds[g];
         newval = old > 0.0 ? 0.0 : old;
         touched = true;
       } else if (fast) {
         // certain hit / miss: the reference's fp64 update, bit for bit
-        double value = dadd(A.log_odds[g], fast == 1 ? A.l_hit : A.l_miss);
+        double value = dadd(old, fast == 1 ? A.l_hit : A.l_miss);
         if (value < A.l_min) value = A.l_min;
         else if (value > A.l_max) value = A.l_max;
         newval = value;
@@ -470,7 +486,7 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
         slot = __shfl_sync(kFull, slot, 0);
         if (slot < A.journal.capacity) {
           const bool inz = z < A.gz;
-          A.journal.lo[slot * 32 + lane] = inz ? A.log_odds[g] : 0.0;
+          A.journal.lo[slot * 32 + lane] = inz ? (in_box ? old : A.log_odds[g]) : 0.0;
           A.journal.ob[slot * 32 + lane] = inz ? A.observed[g] : 0;
           if (lane == 0) {
             A.journal.idx[slot] = (x * A.gy + y) * A.words_z + wz;  // word index of the grid
@@ -507,6 +523,7 @@ __global__ void __launch_bounds__(256) fuse_kernel(const __grid_constant__ Fusio
 struct MaskPixArgs {
   const double *depth;
   uint8_t *out;
+  float *out_f;  // optional: (float)depth where usable, NaN elsewhere (the fusion's one-load pixel test)
   int64_t width, height;
   double fx, fy, cx, cy, d_min, d_max;
   double r[9], t[3];
@@ -526,6 +543,8 @@ struct MaskPixArgs {
 
 // vp/mapping.py:357-380, one thread per pixel.
 __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constant__ MaskPixArgs A) {
+  pdl_release();
+  pdl_wait();
   if (A.j_count != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
     if (A.j_reset) *A.j_count = 0ull;
     if (A.j_starts != nullptr) A.j_starts[A.j_seg] = (int64_t)*A.j_count;
@@ -555,6 +574,7 @@ __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constan
   }
   const uint8_t code = px ? (inside ? 1 : (valid ? 2 : 0)) : 0;
   if (px) A.out[idx] = A.encode_usable ? code : inside;
+  if (px && A.out_f) A.out_f[idx] = code == 2 ? (float)d : __int_as_float(0x7fc00000);
   if (A.bbox) {
     // rectangle of the usable pixels: CTA reduction, then the last CTA
     // (ticket) reduces the CTA rectangles -- no atomics on the rectangle and
@@ -694,7 +714,8 @@ int vpb_occ_bits_from_log_odds(const vpb_grid *grid, double thr, void *stream) {
 
 static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const double *centers,
                               const double *radii, int64_t n_mask, double pad, uint8_t *out, int encode,
-                              int *bbox, void *stream, const vpb_journal *journal = nullptr) {
+                              int *bbox, void *stream, const vpb_journal *journal = nullptr,
+                              float *pixf = nullptr) {
   VPB_REQUIRE(depth && cam && out, "null argument to vpb_masked_pixels");
   MaskPixArgs A;
   memset(&A, 0, sizeof(A));
@@ -704,6 +725,7 @@ static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const 
   for (int64_t s = 0; s < n_mask; ++s) A.mr[s] = radii[s];
   A.depth = depth;
   A.out = out;
+  A.out_f = pixf;
   A.width = cam->width;
   A.height = cam->height;
   A.fx = cam->fx; A.fy = cam->fy; A.cx = cam->cx; A.cy = cam->cy;
@@ -733,14 +755,14 @@ static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const 
     }
     return VPB_OK;
   }
-  masked_pixels_kernel<<<(unsigned)ceil_div(npx, 256), 256, 0, as_stream(stream)>>>(A);
+  VPB_CUDA(launch_pdl(masked_pixels_kernel, dim3((unsigned)ceil_div(npx, 256)), dim3(256), 0, as_stream(stream), A));
   return check_launch("masked_pixels_kernel");
 }
 
 static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
                      const double *depth, const uint8_t *pixel_masked, const double *centers,
                      const double *radii, int64_t n_mask, const vpb_map_params *p, int usable, const int *bbox,
-                     void *stream, const vpb_journal *journal = nullptr) {
+                     void *stream, const vpb_journal *journal = nullptr, const float *pixf = nullptr) {
   VPB_REQUIRE(grid && grid->log_odds && grid->observed && cam && depth && pixel_masked && p,
               "null argument to vpb_fuse_voxels");
   for (int k = 0; k < 3; ++k)
@@ -801,6 +823,7 @@ static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
   A.width = cam->width; A.height = cam->height;
   A.depth = depth;
   A.pixel_masked = pixel_masked;
+  A.pixf = pixf;
   A.tau = p->tau; A.l_hit = p->l_hit; A.l_miss = p->l_miss;
   A.l_min = p->l_min; A.l_max = p->l_max; A.l_thr = p->l_occ_threshold;
   A.n_mask = (int)n_mask;
@@ -859,7 +882,7 @@ static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
   static const int per_sm_env = getenv("VPB_FUSE_CTAS_PER_SM") ? atoi(getenv("VPB_FUSE_CTAS_PER_SM")) : 0;
   const int64_t slots = (int64_t)sm_count() * (per_sm_env > 0 ? per_sm_env : (occ > 0 ? occ : 4));
   const int64_t ctas = max_ctas < slots ? max_ctas : slots;
-  fuse_kernel<<<(unsigned)ctas, 256, 0, as_stream(stream)>>>(A);
+  VPB_CUDA(launch_pdl(fuse_kernel, dim3((unsigned)ctas), dim3(256), 0, as_stream(stream), A));
   return check_launch("fuse_kernel");
 }
 
@@ -874,9 +897,14 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3
   return fuse_impl(grid, lo, n, cam, depth, pixel_masked, centers, radii, n_mask, p, 0, nullptr, stream);
 }
 
+// pixel scratch: [class byte per pixel | bbox (8 ints) | 8 ints per masked-pixels CTA | fp32 depth per pixel]
+static size_t pixf_offset(int64_t npx) {
+  return align_up(align_up((size_t)npx, 16) + 32 + 32 * (size_t)ceil_div(npx > 0 ? npx : 1, 256) + 64, 16);
+}
+
 int64_t vpb_pixel_scratch_bytes(int64_t width, int64_t height) {
   const int64_t npx = width * height;
-  return (int64_t)align_up((size_t)npx, 16) + 32 + 32 * ceil_div(npx > 0 ? npx : 1, 256) + 64;
+  return (int64_t)pixf_offset(npx) + 4 * npx;
 }
 
 int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3], const vpb_camera *cam,
@@ -896,9 +924,12 @@ int vpb_update_occupancy_journaled(const vpb_grid *grid, const int64_t lo[3], co
   // return; followed by the bounding rectangle of the usable pixels
   const int64_t npx = cam->width * cam->height;
   int *bbox = reinterpret_cast<int *>(pixel_scratch + align_up((size_t)npx, 16));
-  int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, bbox, stream, journal);
+  float *pixf = reinterpret_cast<float *>(pixel_scratch + pixf_offset(npx));
+  int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, bbox, stream, journal,
+                              pixf);
   if (rc) return rc;
-  return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, bbox, stream, journal);
+  return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, bbox, stream, journal,
+                   pixf);
 }
 
 int vpb_journal_restore(const vpb_grid *grid, const vpb_journal *j, int64_t first, int64_t last, void *stream) {
