@@ -98,10 +98,11 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3],
 
 /* Masked pixels + fusion in one call: vp/mapping.py:386-455
  * (update_occupancy).  pixel_scratch (dev) holds
- * vpb_pixel_scratch_bytes(W, H) bytes: a per-pixel class byte, the bounding
- * rectangle of the usable pixels (used to skip whole voxel ranges) and its
- * per-CTA reduction; ZERO-initialise it once at allocation (a ticket counter
- * inside it returns to zero at the end of every call). */
+ * vpb_pixel_scratch_bytes(W, H) bytes: a per-pixel class byte, two slots for
+ * the bounding rectangle of the usable pixels (used to skip whole voxel
+ * ranges; consecutive calls on one scratch alternate between them, each call
+ * clearing the other) and the usable depth per pixel in fp32.  ZERO-initialise
+ * it once at allocation; calls sharing a scratch must be stream-ordered. */
 int64_t vpb_pixel_scratch_bytes(int64_t width, int64_t height);
 int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3],
                          const int64_t n[3], const vpb_camera *cam,

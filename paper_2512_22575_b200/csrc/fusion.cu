@@ -15,6 +15,8 @@
 // voxels whose projection misses the image touch no memory at all.
 #include <climits>
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 
 #include "vpb_common.cuh"
 
@@ -141,11 +143,11 @@ struct Frustum {
 __device__ void frustum_setup(const FusionArgs &A, Frustum &F) {
   int u0 = 0, u1 = -1, v0 = 0, v1 = -1;
   float dmax = 0.0f;
-  if (A.bbox) {
-    u0 = __ldcg(A.bbox + 0);
-    u1 = __ldcg(A.bbox + 1);
-    v0 = __ldcg(A.bbox + 2);
-    v1 = __ldcg(A.bbox + 3);
+  if (A.bbox) {  // zero-identity max encoding (masked_pixels_kernel)
+    u0 = (int)A.width - __ldcg(A.bbox + 0);
+    u1 = __ldcg(A.bbox + 1) - 1;
+    v0 = (int)A.height - __ldcg(A.bbox + 2);
+    v1 = __ldcg(A.bbox + 3) - 1;
     dmax = __int_as_float(__ldcg(A.bbox + 4));
   }
   float lo[3] = {1e30f, 1e30f, 1e30f}, hi[3] = {-1e30f, -1e30f, -1e30f};
@@ -529,9 +531,13 @@ struct MaskPixArgs {
   double r[9], t[3];
   int n_mask;
   int encode_usable;  // out = 1 masked, 2 usable return, 0 otherwise
-  int *bbox;          // optional: [umin, umax, vmin, vmax] of usable pixels
-  int *partials;      // per-CTA rectangles (bbox != null)
-  unsigned *counter;  // CTA ticket, zero between launches (the last CTA resets it)
+  // optional: the usable pixels' rectangle and farthest return, reduced by
+  // atomicMax into bbox as [W - umin, umax + 1, H - vmin, vmax + 1, dmax bits]
+  // (zero = empty, so a zeroed slot is the identity); bbox_next is the other
+  // slot of the pair, consumed by the previous call's fusion: zeroed here for
+  // the next call (no ticket, no last-CTA pass, no memset)
+  unsigned *bbox;
+  unsigned *bbox_next;
   // journal segment bookkeeping (vpb_journal.starts / seg / reset), before fusion's first record
   unsigned long long *j_count;
   int64_t *j_starts;
@@ -576,19 +582,15 @@ __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constan
   if (px) A.out[idx] = A.encode_usable ? code : inside;
   if (px && A.out_f) A.out_f[idx] = code == 2 ? (float)d : __int_as_float(0x7fc00000);
   if (A.bbox) {
-    // rectangle of the usable pixels: CTA reduction, then the last CTA
-    // (ticket) reduces the CTA rectangles -- no atomics on the rectangle and
-    // no memset before the launch
-    // plus the farthest usable return (float bits rounded up: positive
-    // floats order like their bit patterns)
-    __shared__ int red[5][8];
-    __shared__ unsigned last;
+    __shared__ unsigned red[5][8];
+    if (blockIdx.x == 0 && threadIdx.x < 5) A.bbox_next[threadIdx.x] = 0u;
     const bool use = code == 2;
-    int r0 = __reduce_min_sync(kFull, use ? (int)uu : INT_MAX);
-    int r1 = __reduce_max_sync(kFull, use ? (int)uu : INT_MIN);
-    int r2 = __reduce_min_sync(kFull, use ? (int)vv : INT_MAX);
-    int r3 = __reduce_max_sync(kFull, use ? (int)vv : INT_MIN);
-    int r4 = __reduce_max_sync(kFull, use ? __float_as_int(__double2float_ru(d)) : 0);
+    // (float bits of a non-negative depth rounded up order like the depths)
+    const unsigned r0 = __reduce_max_sync(kFull, use ? (unsigned)(A.width - uu) : 0u);
+    const unsigned r1 = __reduce_max_sync(kFull, use ? (unsigned)(uu + 1) : 0u);
+    const unsigned r2 = __reduce_max_sync(kFull, use ? (unsigned)(A.height - vv) : 0u);
+    const unsigned r3 = __reduce_max_sync(kFull, use ? (unsigned)(vv + 1) : 0u);
+    const unsigned r4 = __reduce_max_sync(kFull, use ? __float_as_uint(fmaxf(__double2float_ru(d), 0.0f)) : 0u);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (lane == 0) {
       red[0][warp] = r0;
@@ -598,40 +600,10 @@ __global__ void __launch_bounds__(256) masked_pixels_kernel(const __grid_constan
       red[4][warp] = r4;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
-        r0 = min(r0, red[0][w]);
-        r1 = max(r1, red[1][w]);
-        r2 = min(r2, red[2][w]);
-        r3 = max(r3, red[3][w]);
-        r4 = max(r4, red[4][w]);
-      }
-      int *pp = A.partials + 8 * blockIdx.x;
-      pp[0] = r0, pp[1] = r1, pp[2] = r2, pp[3] = r3, pp[4] = r4;
-      __threadfence();
-      last = atomicAdd(A.counter, 1u) == gridDim.x - 1 ? 1u : 0u;
-    }
-    __syncthreads();
-    if (last && threadIdx.x < 32) {
-      __threadfence();
-      int m0 = INT_MAX, m1 = INT_MIN, m2 = INT_MAX, m3 = INT_MIN, m4 = 0;
-      for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
-        const int *pp = A.partials + 8 * b;
-        m0 = min(m0, __ldcg(pp + 0));
-        m1 = max(m1, __ldcg(pp + 1));
-        m2 = min(m2, __ldcg(pp + 2));
-        m3 = max(m3, __ldcg(pp + 3));
-        m4 = max(m4, __ldcg(pp + 4));
-      }
-      m0 = __reduce_min_sync(kFull, m0);
-      m1 = __reduce_max_sync(kFull, m1);
-      m2 = __reduce_min_sync(kFull, m2);
-      m3 = __reduce_max_sync(kFull, m3);
-      m4 = __reduce_max_sync(kFull, m4);
-      if (threadIdx.x == 0) {
-        A.bbox[0] = m0, A.bbox[1] = m1, A.bbox[2] = m2, A.bbox[3] = m3, A.bbox[4] = m4;
-        *A.counter = 0u;
-      }
+    if (threadIdx.x < 5) {
+      unsigned m = 0u;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = max(m, red[threadIdx.x][w]);
+      if (m != 0u) atomicMax(A.bbox + threadIdx.x, m);
     }
   }
 }
@@ -715,7 +687,7 @@ int vpb_occ_bits_from_log_odds(const vpb_grid *grid, double thr, void *stream) {
 static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const double *centers,
                               const double *radii, int64_t n_mask, double pad, uint8_t *out, int encode,
                               int *bbox, void *stream, const vpb_journal *journal = nullptr,
-                              float *pixf = nullptr) {
+                              float *pixf = nullptr, int *bbox_pair = nullptr) {
   VPB_REQUIRE(depth && cam && out, "null argument to vpb_masked_pixels");
   MaskPixArgs A;
   memset(&A, 0, sizeof(A));
@@ -734,10 +706,9 @@ static int masked_pixels_impl(const double *depth, const vpb_camera *cam, const 
   memcpy(A.t, cam->pose_t, sizeof(A.t));
   A.n_mask = (int)n_mask;
   A.encode_usable = encode;
-  A.bbox = bbox;
-  if (bbox) {  // [u0 u1 v0 v1 dmax_bits - ticket -] then 8 ints per CTA
-    A.counter = reinterpret_cast<unsigned *>(bbox + 6);
-    A.partials = bbox + 8;
+  if (bbox) {  // slot pair [8 ints][8 ints]: this call's and the next call's
+    A.bbox = reinterpret_cast<unsigned *>(bbox);
+    A.bbox_next = reinterpret_cast<unsigned *>(bbox == bbox_pair ? bbox_pair + 8 : bbox_pair);
   }
   A.pad = pad;
   if (journal != nullptr && journal->count != nullptr) {
@@ -897,7 +868,9 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3], const int64_t n[3
   return fuse_impl(grid, lo, n, cam, depth, pixel_masked, centers, radii, n_mask, p, 0, nullptr, stream);
 }
 
-// pixel scratch: [class byte per pixel | bbox (8 ints) | 8 ints per masked-pixels CTA | fp32 depth per pixel]
+// pixel scratch: [class byte per pixel | 2 rectangle slots of 8 ints (+ spare) | fp32 depth per pixel]
+// (the slot size term is the old per-CTA partial area, kept so the layout of
+// the scratch the callers allocate does not move)
 static size_t pixf_offset(int64_t npx) {
   return align_up(align_up((size_t)npx, 16) + 32 + 32 * (size_t)ceil_div(npx > 0 ? npx : 1, 256) + 64, 16);
 }
@@ -923,10 +896,19 @@ int vpb_update_occupancy_journaled(const vpb_grid *grid, const int64_t lo[3], co
   // pixel classes in one byte: 1 = return on the robot body, 2 = usable
   // return; followed by the bounding rectangle of the usable pixels
   const int64_t npx = cam->width * cam->height;
-  int *bbox = reinterpret_cast<int *>(pixel_scratch + align_up((size_t)npx, 16));
+  int *pair = reinterpret_cast<int *>(pixel_scratch + align_up((size_t)npx, 16));
+  // the slot of this call alternates per scratch buffer (stream-ordered calls)
+  unsigned parity;
+  {
+    static std::mutex mu;
+    static std::unordered_map<const void *, unsigned> calls;
+    std::lock_guard<std::mutex> lk(mu);
+    parity = calls[pair]++ & 1u;
+  }
+  int *bbox = pair + 8 * parity;
   float *pixf = reinterpret_cast<float *>(pixel_scratch + pixf_offset(npx));
   int rc = masked_pixels_impl(depth, cam, centers, radii, n_mask, mask_pad, pixel_scratch, 1, bbox, stream, journal,
-                              pixf);
+                              pixf, pair);
   if (rc) return rc;
   return fuse_impl(grid, lo, n, cam, depth, pixel_scratch, centers, radii, n_mask, params, 1, bbox, stream, journal,
                    pixf);
