@@ -240,6 +240,45 @@ def test_fusion_random_frames_vs_oracle(M):
     np.testing.assert_array_equal(mapper_field.sq, oracle.edt3d(lo))
 
 
+def test_fusion_rectangle_slots_alternate(M):
+    """The usable-pixel rectangle lives in two scratch slots that alternate per
+    call (each call clears the other): frames whose rectangles shrink, vanish
+    (no valid return) and grow again must each fuse exactly like the oracle."""
+    from paper_2512_22575_b200 import config, robot, scene
+    from paper_2512_22575_b200.geometry import RigidTransform, Rotation3
+
+    chain, model = config.robot_7dof()
+    dims = (64, 64, 80)
+    grid = M.VoxelGrid((-0.64, -0.64, 0.0), 0.02, dims)
+    lo = np.zeros(dims)
+    ob = np.zeros(dims, bool)
+    box = grid.full_box()
+    centers, radii = robot.sphere_positions(chain, np.full(7, 0.2), model)
+    pose = RigidTransform(Rotation3.rot_y(0.1), (0.0, 0.0, -1.0))
+    cam = M.CameraModel(120.0, 118.0, 79.5, 59.5, 160, 120, 0.05, 20.0, pose=pose)
+    boxes = [[((-0.1, -0.1, 0.7), (0.1, 0.1, 0.9))],           # small, near
+             None,                                              # no valid return at all
+             [((-0.6, -0.6, 1.2), (0.6, 0.6, 1.5))],           # wide, far
+             [((0.2, 0.1, 0.8), (0.3, 0.25, 0.95))],           # small, off-centre
+             None,
+             None,
+             [((-0.3, -0.5, 0.9), (0.5, 0.2, 1.3))]]
+    for frame, bx in enumerate(boxes):
+        if bx is None:
+            depth_np = np.zeros((cam.height, cam.width))  # below d_min everywhere
+        else:
+            depth_np = scene.render_boxes(cam, [(np.array(a), np.array(b)) for a, b in bx], (centers, radii))
+        M.update_occupancy(grid, M.DepthImage(depth_np), cam, mask=(centers, radii), volume=box)
+        pm = oracle.masked_pixels(depth_np, cam.fx, cam.fy, cam.cx, cam.cy, cam.d_min, cam.d_max,
+                                  cam.pose.rotation.matrix, cam.pose.translation, centers, radii, 0.01)
+        r, t = cam.world_to_camera()
+        oracle.fuse_voxels(lo, ob, box.lo, box.shape, grid.origin, grid.voxel_size, r, t, cam.fx, cam.fy, cam.cx,
+                           cam.cy, cam.width, cam.height, cam.d_min, cam.d_max, depth_np, pm, centers, radii,
+                           grid.tau, 0.85, -0.4, -2.0, 3.5)
+        np.testing.assert_array_equal(grid.log_odds_host(), lo, err_msg=f"frame {frame}")
+        np.testing.assert_array_equal(grid.observed_host(), ob, err_msg=f"frame {frame}")
+
+
 def test_mapper_pipeline_256_masked(M):
     """C2 pipeline (bench scene 256^3 + 7-DoF mask): fusion + EDT from the
     maintained mask equal the oracle bit for bit."""
