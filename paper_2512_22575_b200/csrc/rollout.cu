@@ -41,7 +41,10 @@ namespace vpb {
 constexpr int NW = 8;                    // candidate warps per CTA (generic path, rollout kernel)
 constexpr int NWF = 4;                   // candidate warps per CTA of the fixed-topology SMPC kernel
 constexpr int kThreads = (NW + 1) * 32;  // + terminal warp
-#define VPB_NOM_INLINE 512  // H n of the parameter-carried nominal (session path)
+// H n of the parameter-carried nominal (session path; larger H n take the
+// staged-block session).  The launch cost grows with the parameter block
+// (~0.4 us per KB on the C3 step): 256 covers C1/C3/C5 (H n = 140 / 224).
+#define VPB_NOM_INLINE 256
 constexpr int kPartHead = 4;             // [m, Z, nonfinite, best_index]
 constexpr int kPartExt = 7;              // after N: [nonzero-weight count, the single candidate's 6 sums]
 constexpr int kGroup = 32;               // CTAs merged by a group's last CTA

@@ -477,12 +477,13 @@ def test_fixed_topology_equals_generic(pk, precision, monkeypatch):
             np.testing.assert_allclose(s0[:base + 11], s1[:base + 11], rtol=1e-9, atol=1e-9)
 
 
-@pytest.mark.parametrize("precision", ["fp32", "fp64"])
-def test_native_session_equals_device_step(pk, precision):
+@pytest.mark.parametrize("precision,horizon", [("fp32", 24), ("fp64", 24), ("fp32", 48)])
+def test_native_session_equals_device_step(pk, precision, horizon):
     """vpb_smpc_session (one host call: staged block, captured graph of
     sampler + fused step, host diagnostics) returns exactly the device step
     on the same seed, follows a field rebuilt into a new buffer, and fills
-    e_pos / e_ori like the reference (vp/planner.py:620-629)."""
+    e_pos / e_ori like the reference (vp/planner.py:620-629).  H = 48 puts
+    H n past the launch-parameter nominal (the session's staged-block path)."""
     pkg, config, mapping, planner, robot = pk
     from paper_2512_22575_b200.geometry import RigidTransform, quaternion_angle
 
@@ -496,16 +497,16 @@ def test_native_session_equals_device_step(pk, precision):
     grid.set_log_odds(np.where(occ, 3.5, 0.0))
     f2 = mapping.edt_3d(grid, outside_default=0.8)
     assert f1.sq_device.data_ptr() != f2.sq_device.data_ptr()
-    params = config.planner_params(7, {"samples": 700, "horizon": 24})
+    params = config.planner_params(7, {"samples": 700, "horizon": horizon})
     pl = planner.Planner(chain, model, params, precision)
     state = robot.JointState(np.full(7, 0.1), np.linspace(-0.2, 0.2, 7), np.zeros(7))
     goal = RigidTransform.from_vec7([0.3, -0.2, 0.7, 0.9, 0.1, 0.3, -0.2])
-    nom = 0.2 * np.cos(np.arange(24 * 7)).reshape(24, 7)
+    nom = 0.2 * np.cos(np.arange(horizon * 7)).reshape(horizon, 7)
     for field, seed in ((f1, 5), (f2, 6), (f1, 7)):
         res = pl.smpc_step(state, goal, field, nom, seed)  # native session
         eps = pl.sample_device(seed)
         out = pl.smpc_step_device(state, goal, field, torch.from_numpy(nom).cuda(), eps).cpu().numpy()
-        ref = pl.unpack_step(out, state, goal, 24)
+        ref = pl.unpack_step(out, state, goal, horizon)
         np.testing.assert_array_equal(res.command, ref.command)
         np.testing.assert_array_equal(res.next_nominal, ref.next_nominal)
         assert res.diagnostics.weighted_cost == ref.diagnostics.weighted_cost
