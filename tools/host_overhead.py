@@ -13,6 +13,8 @@ import torch  # noqa: E402
 
 
 def best(fn, n=200):
+    for _ in range(n):  # warm-up pass (CPU clocks, caches): the first timed series ran ~9 us slow
+        fn()
     ts = []
     for _ in range(n):
         t0 = time.perf_counter()
