@@ -38,6 +38,11 @@ int vpb_version(void);
 const char *vpb_last_error(void);
 /* Number of kernels this library has launched since load (diagnostics). */
 uint64_t vpb_launch_count(void);
+/* Host -> device upload through a caller-owned pinned staging buffer: copies
+ * `bytes` from src_host into pinned (on the host, now) and enqueues the
+ * pinned -> dst_dev copy on `stream` (the depth frame of a map update; the
+ * caller must not reuse `pinned` before that copy has run). */
+int vpb_stage_h2d(void *dst_dev, void *pinned, const void *src_host, int64_t bytes, void *stream);
 
 /* ------------------------------------------------------------------------ */
 /* Mapping                                                                   */

@@ -91,6 +91,7 @@ SIGNATURES = {
     "vpb_version": (ctypes.c_int, []),
     "vpb_last_error": (ctypes.c_char_p, []),
     "vpb_launch_count": (ctypes.c_uint64, []),
+    "vpb_stage_h2d": (ctypes.c_int, [_p, _p, _p, _i64, _p]),
     "vpb_occ_words": (_i64, [_P(_i64)]),
     "vpb_occ_bits_from_log_odds": (ctypes.c_int, [_P(VpbGrid), _d, _p]),
     "vpb_masked_pixels": (ctypes.c_int, [_p, _P(VpbCamera), _p, _p, _i64, _d, _p, _p]),

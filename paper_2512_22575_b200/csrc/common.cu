@@ -46,4 +46,12 @@ const char *vpb_last_error(void) { return vpb::g_err; }
 
 uint64_t vpb_launch_count(void) { return vpb::g_launches.load(); }
 
+int vpb_stage_h2d(void *dst_dev, void *pinned, const void *src_host, int64_t bytes, void *stream) {
+  VPB_REQUIRE(bytes >= 0 && (bytes == 0 || (dst_dev && pinned && src_host)), "bad vpb_stage_h2d arguments");
+  if (bytes == 0) return VPB_OK;
+  memcpy(pinned, src_host, (size_t)bytes);
+  VPB_CUDA(cudaMemcpyAsync(dst_dev, pinned, (size_t)bytes, cudaMemcpyHostToDevice, vpb::as_stream(stream)));
+  return VPB_OK;
+}
+
 }  // extern "C"
