@@ -1111,19 +1111,29 @@ __device__ void heavy_sum_slice(const SmpcIO &io, const Shared &S, unsigned int 
   const int Lp = 2 + hn;
   const int per = (hn + P - 1) / P;
   const int e0 = part * per, e1 = min(hn, e0 + per);
-  double *red = reinterpret_cast<double *>(S.centers);  // [nw] (free here)
-  for (int e = e0; e < e1; ++e) {
-    const double v = tid < P ? __ldcg(io.hparts + (size_t)tid * Lp + 2 + e) : 0.0;
-    const double ws = warp_sum_d(v);
-    if (lane == 0) red[warp] = ws;
-    __syncthreads();
-    if (tid == 0) {
+  (void)S;
+  if (P <= 32) {
+    // few partials (a long slice): each thread one element, the P partials
+    // added in participant order, every element of the slice at once
+    for (int e = e0 + tid; e < e1; e += nt) {
+      const double *src = io.hparts + 2 + e;
       double acc = 0.0;
-      for (int w = 0; w < nw; ++w) acc += red[w];  // fixed warp order
+#pragma unroll 8
+      for (int q = 0; q < P; ++q) acc += __ldcg(src + (size_t)q * Lp);
       io.rank_part[kPartHead + e] = acc;
     }
-    __syncthreads();
+  } else {
+    // many partials (a short slice): one warp per element, lane q adds
+    // participants q, q + 32, ... in order, then a fixed xor tree
+    for (int e = e0 + warp; e < e1; e += nw) {
+      const double *src = io.hparts + 2 + e;
+      double v = 0.0;
+      for (int q = lane; q < P; q += 32) v += __ldcg(src + (size_t)q * Lp);
+      const double ws = warp_sum_d(v);
+      if (lane == 0) io.rank_part[kPartHead + e] = ws;
+    }
   }
+  __syncthreads();  // the slice is written before this participant counts itself
   if (tid == 0) {
     fence_acq_rel_gpu();
     atomicAdd(hc + kHcDone2, 1u);
@@ -1406,9 +1416,11 @@ __device__ void final_merge(const SmpcIO &io, const Shared &S, const double *hea
       hc[kHcSpan] = (unsigned int)span;
       hc[kHcNw] = (unsigned int)nw;
       hc[kHcList] = (unsigned int)(ncand / NWC);
-      // about nt / 2 candidates per participant: the slice's row loads take a
-      // few round trips while the partials to add stay few
-      const int want = (ncand + nt / 2 - 1) / (nt / 2);
+      // about nt / 8 candidates per participant: the slice's row loads take
+      // two round trips; the partials are added per element in parallel
+      // (heavy_sum_slice), so more participants cost little (r2: converged
+      // C3 step 71.7 -> 59.6 us, converged M = 256 80.6 -> 55.3 us)
+      const int want = (ncand + nt / 8 - 1) / (nt / 8);
       hc[kHcParts] = (unsigned int)(want < ph + 1 ? (want > 1 ? want : 1) : ph + 1);
       fence_acq_rel_gpu();  // helpers read the lists and these words after this release
     }
