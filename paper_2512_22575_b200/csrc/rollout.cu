@@ -986,20 +986,27 @@ __device__ __forceinline__ int merge_helpers(const SmpcIO &io, int ctas) {
 // elements, candidates in list order) -> hparts[part].  The merger then adds
 // the participants' partials in participant order: deterministic.
 template <typename ET, int NWC>
-__device__ void heavy_part(const SmpcIO &io, const Shared &S, const unsigned int *hc, int part, int P, int hn) {
+__device__ void heavy_part(const SmpcIO &io, const Shared &S, const unsigned int *hc, int part, int P, int hn,
+                           unsigned long long *ht = nullptr) {
   const int tid = threadIdx.x, nt = blockDim.x;
   const ET *eps = reinterpret_cast<const ET *>(io.eps);
   const double *costs = io.costs ? io.costs : io.cand_costs;
   double *wlist = io.group_parts;
   int *mlist = reinterpret_cast<int *>(io.group_parts + io.M + 64);
   const int *clist = reinterpret_cast<const int *>(io.group_parts + io.M + 64) + io.M + 64;
-  const unsigned long long m0b = (unsigned long long)__ldcg(hc + kHcM0) | ((unsigned long long)__ldcg(hc + kHcM0 + 1) << 32);
+  // the verdict words once per CTA (every thread of ~128 participants loading
+  // them from the one L2 line serialised the helpers: r2, 16k-candidate merge
+  // helper parts 18 -> ~2 us)
+  __shared__ unsigned int hcw[kHcParts - kHcM0];
+  if (tid < kHcParts - kHcM0) hcw[tid] = __ldcg(hc + kHcM0 + tid);
+  __syncthreads();
+  const unsigned long long m0b = (unsigned long long)hcw[0] | ((unsigned long long)hcw[1] << 32);
   const double m0 = __longlong_as_double((long long)m0b);
   const double inv_lam = 1.0 / io.lam;
-  const int span = (int)__ldcg(hc + kHcSpan), nw = (int)__ldcg(hc + kHcNw), list = (int)__ldcg(hc + kHcList);
+  const int span = (int)hcw[kHcSpan - kHcM0], nw = (int)hcw[kHcNw - kHcM0], list = (int)hcw[kHcList - kHcM0];
   int wc[16];
 #pragma unroll
-  for (int w = 0; w < 16; ++w) wc[w] = w < nw ? (int)__ldcg(hc + kHcWcount + w) : 0;
+  for (int w = 0; w < 16; ++w) wc[w] = w < nw ? (int)hcw[kHcWcount - kHcM0 + w] : 0;
   const int per = (list + P - 1) / P;
   const int j0 = part * per, j1 = min(list, j0 + per);
   constexpr int kE = 2;  // N elements per thread and pass (passes over blocks of kE nt elements)
@@ -1041,6 +1048,7 @@ __device__ void heavy_part(const SmpcIO &io, const Shared &S, const unsigned int
     }
     __syncthreads();
     const int cnt = min(nt, NWC * j1 - k0);
+    if (ht && tid == 0 && k0 == NWC * j0) ht[1] = gtimer();
     if (tid == 0) {
       for (int w = 0; w < (nt >> 5); ++w) {
         z += wred[w];
@@ -1152,12 +1160,17 @@ __device__ void merge_helper(const SmpcIO &io, const Shared &S, int ctas, int hn
     while (((f = ld_acquire_gpu(c + kHcFlag)) >> 2) != (ep & 0x3fffffffu) || (f & 3u) == 0u) g.pause(512);
     st[0] = f & 3u;
     st[1] = ld_acquire_gpu(c + kHcCount);
+    st[2] = (f & 3u) == 2u ? __ldcg(c + kHcParts) : 0u;
   }
   __syncthreads();
   if (st[0] != 2u) return;
-  const int P = (int)__ldcg(c + kHcParts);  // participants: helpers 0 .. P-2 and the merger
+  const int P = (int)st[2];  // participants: helpers 0 .. P-2 and the merger
   if (part >= P - 1) return;
-  heavy_part<ET, NWC>(io, S, c, part, P, hn);
+  // (tools/smpc_trace.py: per-helper stamps after the fixed slots)
+  unsigned long long *ht = io.trace ? io.trace + 2 * ctas + 32 + 3 * part : nullptr;
+  if (ht && threadIdx.x == 0) ht[0] = gtimer();
+  heavy_part<ET, NWC>(io, S, c, part, P, hn, ht);  // ht[1]: weights of the first chunk done
+  if (ht && threadIdx.x == 0) ht[2] = gtimer();
   heavy_sum_slice(io, S, c, part, P, hn);
 }
 

@@ -12,6 +12,11 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 
+def _pct(v, t0):
+    v = v[v > 0]
+    return [float(np.percentile(v - t0, p)) / 1e3 for p in (0, 50, 100)] if v.size else []
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--samples", type=int, default=4096)
@@ -54,7 +59,7 @@ def main():
         nom = torch.zeros((a.horizon, 7), dtype=torch.float64, device="cuda")
     eps = pl.sample_device(3)
     ctas = (a.samples + 3) // 4  # fixed-topology path: 4 candidates per CTA
-    buf = torch.zeros(2 * ctas + 32, dtype=torch.int64, device="cuda")
+    buf = torch.zeros(2 * ctas + 32 + 3 * 128, dtype=torch.int64, device="cuda")
     for _ in range(5):
         pl.smpc_step_device(st, goal, field, nom, eps)
     torch.cuda.synchronize()
@@ -97,6 +102,14 @@ def main():
             "heavy_helpers_done_us": (t[2 * ctas + 22] - t0) / 1e3,
             "heavy_sums_done_us": (t[2 * ctas + 23] - t0) / 1e3,
             "slowest_ctas": [int(i) for i in np.argsort(done)[-6:]],
+            # heavy merge, per helper that took part: woke (saw the verdict), first weights done, own part done
+            "helper_woke_us": _pct(t[2 * ctas + 32::3], t0),
+            "helper_weights_done_us": _pct(t[2 * ctas + 33::3], t0),
+            "helper_part_done_us": _pct(t[2 * ctas + 34::3], t0),
+            "helper_weights_dur_by_part_us": [round(float(b - a) / 1e3, 2) for a, b in
+                                              zip(t[2 * ctas + 32::3], t[2 * ctas + 33::3]) if a > 0][:128],
+            "helper_part_dur_by_part_us": [round(float(b - a) / 1e3, 2) for a, b in
+                                           zip(t[2 * ctas + 32::3], t[2 * ctas + 34::3]) if a > 0][:128],
             "done_by_cta_decile_us": [float(np.median(d)) / 1e3 for d in np.array_split(done, 10)],
         })
     out = dict(res[-1])
