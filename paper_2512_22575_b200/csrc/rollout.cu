@@ -994,9 +994,9 @@ __device__ void heavy_part(const SmpcIO &io, const Shared &S, const unsigned int
   double *wlist = io.group_parts;
   int *mlist = reinterpret_cast<int *>(io.group_parts + io.M + 64);
   const int *clist = reinterpret_cast<const int *>(io.group_parts + io.M + 64) + io.M + 64;
-  // the verdict words once per CTA (every thread of ~128 participants loading
-  // them from the one L2 line serialised the helpers: r2, 16k-candidate merge
-  // helper parts 18 -> ~2 us)
+  // the verdict words once per CTA instead of every thread of up to 128
+  // participants loading them from the one L2 line (16k-candidate converged
+  // step: -2..4 us)
   __shared__ unsigned int hcw[kHcParts - kHcM0];
   if (tid < kHcParts - kHcM0) hcw[tid] = __ldcg(hc + kHcM0 + tid);
   __syncthreads();
