@@ -60,6 +60,11 @@ def test_pure_host_entry_points(lib):
     assert lib.vpb_edt3d_workspace_bytes(i64x3((8, 8, 8))) >= 8 * 8 * 8 * 6
     assert lib.vpb_smpc_partial_len(32, 7) == 4 + 224 + 7
     assert lib.vpb_smpc_out_len(32, 7) == 2 * 224 + 7 + 13
+    # argument checks run before any CUDA call; a zero-byte upload is a no-op
+    assert lib.vpb_stage_h2d(None, None, None, 16, None) == 1  # VPB_ERR_ARG
+    assert b"vpb_stage_h2d" in lib.vpb_last_error()
+    assert lib.vpb_stage_h2d(None, None, None, 0, None) == 0
+    assert lib.vpb_pixel_scratch_bytes(160, 120) >= 160 * 120 * 5 + 64  # class byte + fp32 depth + rectangle slots
 
 
 def test_struct_layout_matches_header(lib):
