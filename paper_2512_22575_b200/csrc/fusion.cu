@@ -44,6 +44,7 @@ struct FusionArgs {
   int usable;  // pixel_masked carries bit1 = usable return (vpb_update_occupancy)
   const int *bbox;  // optional bounding rectangle of usable pixels (chunk early-out)
   float tauf;
+  float inv_fx, inv_fy, inv_vox;  // reciprocals for the (margin-padded) frustum footprint
   float bb_lo[3], bb_hi[3];
   // frustum culling (fp32, conservative): camera centre and camera->world
   // rotation, voxel-index box of the mask spheres (empty if none)
@@ -129,8 +130,9 @@ struct Interval {
 
 __device__ __forceinline__ void clip_lin(float a, float b, float &zlo, float &zhi) {
   // keep z with a + b z >= 0
-  if (b > 0.0f) zlo = fmaxf(zlo, -a / b);
-  else if (b < 0.0f) zhi = fminf(zhi, -a / b);
+  // (__fdividef: <= 2 ulp, next to the intervals' 2-voxel widening)
+  if (b > 0.0f) zlo = fmaxf(zlo, __fdividef(-a, b));
+  else if (b < 0.0f) zhi = fminf(zhi, __fdividef(-a, b));
   else if (a < 0.0f) zhi = -1e30f;
 }
 
@@ -170,7 +172,7 @@ __device__ void frustum_setup(const FusionArgs &A, Frustum &F) {
       for (int k = 0; k < 3; ++k) lo[k] = hi[k] = A.camc[k];
       for (int c = 0; c < 4; ++c) {
         const float u = c & 1 ? F.uhi : F.ulo, v = c & 2 ? F.vhi : F.vlo;
-        const float dc[3] = {(u - (float)A.cx) / A.fxf * F.dfar, (v - (float)A.cy) / A.fyf * F.dfar, F.dfar};
+        const float dc[3] = {(u - (float)A.cx) * A.inv_fx * F.dfar, (v - (float)A.cy) * A.inv_fy * F.dfar, F.dfar};
         for (int k = 0; k < 3; ++k) {
           const float w = A.camc[k] + A.c2w[3 * k + 0] * dc[0] + A.c2w[3 * k + 1] * dc[1] + A.c2w[3 * k + 2] * dc[2];
           lo[k] = fminf(lo[k], w);
@@ -191,8 +193,9 @@ __device__ void frustum_setup(const FusionArgs &A, Frustum &F) {
   for (int k = 0; k < 2; ++k) {
     int a = INT_MAX, b = INT_MIN;
     if (F.ok) {
-      const float fa = fmaxf(fminf((lo[k] - org[k]) / A.voxf - 0.5f, 2.0e9f), -2.0e9f);
-      const float fb = fmaxf(fminf((hi[k] - org[k]) / A.voxf - 0.5f, 2.0e9f), -2.0e9f);
+      // (reciprocal products: a few ulp next to the 2-pixel / 2-voxel margins)
+      const float fa = fmaxf(fminf((lo[k] - org[k]) * A.inv_vox - 0.5f, 2.0e9f), -2.0e9f);
+      const float fb = fmaxf(fminf((hi[k] - org[k]) * A.inv_vox - 0.5f, 2.0e9f), -2.0e9f);
       a = (int)floorf(fa) - 2;
       b = (int)ceilf(fb) + 2;
     }
@@ -818,6 +821,9 @@ static int fuse_impl(const vpb_grid *grid, const int64_t lo[3], const int64_t n[
   }
   A.fxf = (float)A.fx;
   A.fyf = (float)A.fy;
+  A.inv_fx = (float)(1.0 / A.fx);
+  A.inv_fy = (float)(1.0 / A.fy);
+  A.inv_vox = (float)(1.0 / A.voxel);
   A.cxh = (float)(A.cx + 0.5);
   A.cyh = (float)(A.cy + 0.5);
   A.ku = 10.0f * fabsf(A.fxf);
