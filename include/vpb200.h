@@ -107,7 +107,9 @@ int vpb_fuse_voxels(const vpb_grid *grid, const int64_t lo[3],
  * the bounding rectangle of the usable pixels (used to skip whole voxel
  * ranges; consecutive calls on one scratch alternate between them, each call
  * clearing the other) and the usable depth per pixel in fp32.  ZERO-initialise
- * it once at allocation; calls sharing a scratch must be stream-ordered. */
+ * it once at allocation; calls sharing a scratch must be stream-ordered.  (A
+ * CUDA graph that captures the call replays one slot: the rectangle then only
+ * grows -- the result stays exact, the culling gets looser.) */
 int64_t vpb_pixel_scratch_bytes(int64_t width, int64_t height);
 int vpb_update_occupancy(const vpb_grid *grid, const int64_t lo[3],
                          const int64_t n[3], const vpb_camera *cam,
